@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the MoE-layer hot path (BASELINE.json metric, config 2).
+
+Workload (BASELINE.json configs[1]): one Qwen3-30B-A3B MoE layer
+(E=128, top-8, H=2048, I=768) over a hybrid batch of 64 decode + 512 prefill
+tokens = T=576 routed tokens, random-init bf16 weights, synthetic dyadic
+inputs. One "step" = one full layer forward (router, top-k, permute, grouped
+expert FFN, combine). Eight distinct layer weight sets (9.7 GB) are rotated
+step to step, so every step streams its expert weights from HBM (inputs far
+larger than the 126 MB L2).
+
+  value  : device-timed µs per layer step, inputs resident in HBM (lower is better)
+  e2e    : the same through GpuMoE.forward_host with pinned host x / y, H2D+D2H inside
+  roofline: dominant kernel (k_experts) vs measured HBM copy bandwidth
+  cpu_baseline: the fp32 oracle port timed on this host's cores
+
+Multi-GPU (torchrun, N>1): each rank runs its own T=576 batch (tokens
+data-parallel) with the experts it owns (expert-parallel, E/N per rank) and
+NCCL all-to-all dispatch/return (paper_2510_08055_b200.ep); value = max over
+ranks of the per-step time, "scaling": "weak".
+
+`--impl reference` times the reference's CPU path for the same workload
+(the oracle port of the layer; the reference has no numerical layer) on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer us/iter (Qwen3-30B-A3B, 64 decode + 512 prefill tokens)"
+UNIT = "us/iter"
+T_DECODE, T_PREFILL = 64, 512
+N_LAYER_SETS = 8
+N_INPUTS = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--tokens", type=int, default=T_DECODE + T_PREFILL)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.th.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_layer_inputs(T: int, seed: int = 0):
+    from paper_2510_08055_b200 import QWEN3_30B_A3B as s
+    from paper_2510_08055_b200.synthetic import expert_weights, router_tokens, router_weight
+
+    wr = router_weight(s.num_experts, s.hidden, seed).float().numpy()
+    w13, w2 = expert_weights(s.num_experts, s.hidden, s.ffn, seed + 1)
+    x = router_tokens(T, s.hidden, seed + 2).float().numpy()
+    return x, wr, w13.float().numpy(), w2.float().numpy(), s
+
+
+def time_cpu_oracle(T: int, seconds: float, max_iters: int | None = None):
+    """The oracle port of the layer on all host cores: µs per layer forward."""
+    import torch
+
+    from oracle import moe_oracle
+
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    x, wr, w13, w2, s = cpu_layer_inputs(T)
+    moe_oracle.moe_forward(x, wr, w13, w2, s.top_k, s.norm_topk_prob)  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    while (max_iters is None and time.perf_counter() < t_end) or (max_iters is not None and len(times) < max_iters):
+        t0 = time.perf_counter()
+        moe_oracle.moe_forward(x, wr, w13, w2, s.top_k, s.norm_topk_prob)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times) * 1e6, cores, len(times)
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    T = args.tokens
+    from oracle import moe_oracle
+
+    x, wr, w13, w2, s = cpu_layer_inputs(T)
+    for _ in range(args.warmup):
+        moe_oracle.moe_forward(x, wr, w13, w2, s.top_k, s.norm_topk_prob)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        moe_oracle.moe_forward(x, wr, w13, w2, s.top_k, s.norm_topk_prob)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = dt * 1e6
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": f"qwen3-30b-a3b MoE layer, T={T} ({T_DECODE} decode + {T - T_DECODE} prefill)",
+                   "tokens": T, "hidden": 2048, "ffn": 768, "experts": 128, "top_k": 8},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full layer forwards (fp32 numpy oracle, all {cores} host threads; "
+                                   "the reference moesim has no numerical layer, only moe_cost)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args, rank: int, world: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08055_b200 import QWEN3_30B_A3B as s
+    from paper_2510_08055_b200 import _native
+    from paper_2510_08055_b200.moe import GpuMoE
+    from paper_2510_08055_b200.synthetic import router_tokens, router_weight
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    T = args.tokens
+    lib = _native.load()
+
+    if world > 1:
+        from paper_2510_08055_b200.ep import EPMoE
+    layers = []
+    for i in range(N_LAYER_SETS):
+        g = torch.Generator(device=dev).manual_seed(1000 + i)
+        wr = router_weight(s.num_experts, s.hidden, 1000 + i).to(dev)
+        w13 = (torch.randn((s.num_experts, 2 * s.ffn, s.hidden), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        w2 = (torch.randn((s.num_experts, s.hidden, s.ffn), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        if world > 1:
+            layers.append(EPMoE.from_full(s, wr, w13, w2, rank, world))
+        else:
+            layers.append(GpuMoE(s, wr, w13, w2))
+        del g
+    xs = [router_tokens(T, s.hidden, 50 + rank * N_INPUTS + i).to(dev) for i in range(N_INPUTS)]
+    xs_host = [x.cpu().pin_memory() for x in xs]
+    ys = [torch.empty_like(xs[0]) for _ in range(N_INPUTS)]
+    torch.cuda.synchronize()
+
+    def step(i):
+        return layers[i % N_LAYER_SETS](xs[i % N_INPUTS], out=ys[i % N_INPUTS])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warmup
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream) with live stage events
+    stream = torch.cuda.current_stream(dev)
+    K = args.steps
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    for evs in stage_ev:  # materialise the cudaEvent_t handles
+        for e in evs:
+            e.record(stream)
+    torch.cuda.synchronize()
+    ptr_arrays = []
+    for evs in stage_ev:
+        import ctypes
+
+        arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in evs])
+        ptr_arrays.append(arr)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(K):
+            if world == 1:
+                lib.lp_profile_events(ptr_arrays[i], 5)
+            step(i)
+        end.record(stream)
+        torch.cuda.synchronize()
+    lib.lp_profile_events(None, 0)
+    barrier()
+    ms = start.elapsed_time(end) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # per-stage device time (only recorded by the single-GPU fused path)
+    stage_us = None
+    if world == 1:
+        names = ["route", "permute", "experts", "combine"]
+        sums = [0.0] * 4
+        for evs in stage_ev:
+            for j in range(4):
+                sums[j] += evs[j].elapsed_time(evs[j + 1])
+        stage_us = {n: 1e3 * v / K for n, v in zip(names, sums)}
+
+    # ---- end-to-end through the public API with host buffers
+    y_host = torch.empty((T, s.hidden), dtype=torch.bfloat16, pin_memory=True)
+    x_dev = torch.empty((T, s.hidden), dtype=torch.bfloat16, device=dev)
+    for i in range(3):
+        layers[i % N_LAYER_SETS].forward_host(xs_host[i % N_INPUTS], y_host, x_dev=x_dev)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        layers[i % N_LAYER_SETS].forward_host(xs_host[i % N_INPUTS], y_host, x_dev=x_dev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / K
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # routing stats for the roofline (same inputs as the timed steps)
+    hits = []
+    if world == 1:
+        for i in range(N_LAYER_SETS):
+            _, st = layers[i](xs[i % N_INPUTS])
+            hits.append(st.experts_hit)
+    torch.cuda.synchronize()
+
+    if rank != 0:
+        return
+    peak, peak_src = measured_peaks()
+    out = {
+        "metric": METRIC, "value": ms * 1e3, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init Qwen3-30B-A3B-shaped weights, dyadic-grid tokens)",
+        "config": {"workload": f"qwen3-30b-a3b MoE layer, T={T} ({T_DECODE} decode + {T - T_DECODE} prefill)",
+                   "tokens": T, "hidden": s.hidden, "ffn": s.ffn, "experts": s.num_experts, "top_k": s.top_k,
+                   "parallelism": f"ep{world}" if world > 1 else "single",
+                   "l2": f"inputs larger than L2: {N_LAYER_SETS} layer weight sets "
+                         f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
+        "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
+                "d2h_bytes_per_step": T * s.hidden * 2},
+        "gpu_launches": 7 * K,
+        "clocks": clocks.summary(),
+    }
+    if stage_us is not None:
+        nnz = statistics.mean(hits)
+        algo_bytes = nnz * s.bytes_per_expert + 2 * T * s.hidden * 2
+        achieved = algo_bytes / (stage_us["experts"] * 1e-6) / 1e9
+        layer_bytes = nnz * s.bytes_per_expert + s.num_experts * s.hidden * 2 + 2 * T * s.hidden * 2 + T * s.top_k * 8
+        out["roofline"] = {"bound": "hbm", "kernel": "k_experts (grouped gate/up+SiLU*mul and down, tcgen05)",
+                           "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                           "traffic": None, "peak_source": peak_src,
+                           "algo_bytes_per_launch": algo_bytes,
+                           "layer_frac": (layer_bytes / (ms * 1e-3)) / 1e9 / peak}
+        out["stages_us"] = stage_us
+        out["experts_hit_mean"] = nnz
+    if not args.no_cpu_baseline:
+        v, cores, n = time_cpu_oracle(T, args.cpu_seconds)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                               "sample": f"median of {n} full T={T} layer forwards of the fp32 numpy oracle "
+                                         f"(torch/BLAS threads={cores}); reference moesim has no numerical layer"}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

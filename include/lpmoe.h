@@ -1,0 +1,107 @@
+/*
+ * lpmoe.h — C ABI of the B200-native MoE-layer hot path (liblpmoe.so).
+ *
+ * The reference (arxiv 2510.08055 simulator `moesim`) has no numerical MoE
+ * layer: it models the layer with `costmodel.moe_cost` (costmodel.py:57-85),
+ * fed by a `CoverageModel.coverage(routed_tokens, rng)` (coverage.py:216-257)
+ * whose Monte-Carlo backend is `kernels.uniform_union_counts` /
+ * `kernels.weighted_union_counts` (kernels.py:209-222). Those call sites
+ * (engine.py:144-154, cli.py:222-227) are where this library plugs in; each
+ * entry point below names the reference interface it replaces or serves.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers (CUDA global memory), 16-byte
+ *    aligned, row-major, no padding. bf16 tensors are passed as void*.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream), performs no allocation, no host sync and
+ *    no host<->device copy, so a whole layer is CUDA-graph capturable.
+ *  - Return value: LP_OK or an LP_E* code; lp_last_error() gives the text
+ *    (thread-local). Invalid arguments never launch anything.
+ *  - Stateless and reentrant: any host thread may call with its own stream
+ *    and its own workspace.
+ *  - Layouts (HF Qwen3-MoE, transformers 5.5 modeling_qwen3_moe.py:220-224,
+ *    :255): x, y [T,H]; wr [E,H]; w13 [E,2I,H] (gate rows 0..I-1, up rows
+ *    I..2I-1); w2 [E,H,I]. Constraints: H%128==0, I%128==0, E<=256,
+ *    1<=topk<=min(E,32).
+ */
+#ifndef LPMOE_H_
+#define LPMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LP_OK 0
+#define LP_EINVAL 1        /* argument outside the documented domain */
+#define LP_ECUDA 2         /* CUDA runtime/driver error */
+#define LP_EUNSUPPORTED 3  /* valid but not implemented (e.g. E > 256) */
+
+/* Library version string, e.g. "lpmoe 0.1 sm_100a". */
+const char* lp_version(void);
+
+/* Copies the calling thread's last error message into buf (NUL-terminated);
+ * returns the last error code. */
+int lp_last_error(char* buf, size_t n);
+
+/* Bytes of scratch `lp_moe_forward` needs for this shape (>= 0, 256-aligned
+ * regions). Also sufficient for every staged call below. */
+size_t lp_moe_workspace_bytes(int T, int H, int I, int E, int topk);
+
+/* K1 — router + gating. Replaces the routing the reference only models
+ * (coverage.py:140-169 `sample_activation`, kernels.py:73-145): fp32 logits
+ * x.Wr^T, softmax over E, top-k (prob desc, index asc), optional
+ * renormalisation. ids int32 [T,topk], w fp32 [T,topk]. */
+int lp_moe_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids,
+                 float* w, void* ws, size_t ws_bytes, void* stream);
+
+/* K2 — per-expert histogram, offsets (exclusive scan) and stable
+ * permutation. counts [E], offsets [E+1], slot_of [T*topk] (slot of entry
+ * t*topk+j), tok_of [T*topk] (token of slot); x_perm [T*topk,H] gathered rows
+ * (may be NULL to skip the gather). The nnz of `counts` is the measured
+ * coverage the reference's CoverageModel.coverage estimates
+ * (coverage.py:216-257, called at engine.py:147/152). */
+int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
+                   int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* K3 — grouped expert FFN over S expert-contiguous slots (offsets [E+1]):
+ * act = SiLU(x_perm.W13gate^T) * (x_perm.W13up^T) [S,I], y_perm = act.W2^T
+ * [S,H]. tcgen05/TMEM/TMA, one persistent launch. Expert weights of every
+ * expert with >=1 slot are streamed from HBM once per call while
+ * tokens/expert <= the tile cap (the moe_cost byte model, costmodel.py:77). */
+int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void* w13, const void* w2, int H,
+                   int I, int E, void* act, void* y_perm, void* ws, size_t ws_bytes, void* stream);
+
+/* K4 — weighted combine y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]] (bf16 out). */
+int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, int T, int H, int topk, void* y,
+                   void* stream);
+
+/* K1..K4 in one call: y [T,H] bf16 = MoE(x). ids / w / counts may be NULL
+ * (kept in the workspace). Replaces the pair
+ * `coverage_model.coverage(routed)` + `moe_cost(model, routed, cov, 1)` at
+ * engine.py:147-148 / :152-153 with the real layer. */
+int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w2, int T, int H, int I, int E,
+                   int topk, int renorm, void* y, int32_t* ids, float* w, int32_t* counts, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* Routing-surrogate sampler, bit-exact with the reference kernels.
+ * u float64 [trials,batch,k] (C-contiguous), out int64 [trials].
+ * Replaces kernels.uniform_union_counts (kernels.py:209-213, numba body
+ * :73-103) and kernels.weighted_union_counts (kernels.py:216-222, body
+ * :106-145; weights float64 [E]). k <= 64 (uniform), E <= 1024. */
+int lp_union_counts_uniform(const double* u, int trials, int batch, int k, int E, int64_t* out, void* stream);
+int lp_union_counts_weighted(const double* u, int trials, int batch, int k, int E, const double* weights,
+                             int64_t* out, void* stream);
+
+/* Profiling hook (calling thread only): when n >= 5, the next lp_moe_forward
+ * calls record events[0..4] (cudaEvent_t handles) on their stream at the
+ * stage boundaries route | permute | experts | combine | end. n = 0 clears. */
+int lp_profile_events(void* const* events, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPMOE_H_ */

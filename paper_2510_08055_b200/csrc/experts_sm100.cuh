@@ -1,0 +1,295 @@
+// Grouped expert FFN for one MoE layer on sm_100a (tcgen05 + TMEM + TMA).
+//
+// One persistent launch does both expert GEMMs of Qwen3-MoE experts
+// (HF transformers 5.5 `Qwen3MoeExperts.forward`, modeling_qwen3_moe.py:229-249):
+//     act[s, :]    = SiLU(x_perm[s] . W13[e, 0:I]^T) * (x_perm[s] . W13[e, I:2I]^T)
+//     y_perm[s, :] = act[s] . W2[e]^T
+// for every slot s of expert e (slots are expert-contiguous, see permute.cuh).
+//
+// Swap-AB: the weight rows are the MMA M operand (128 rows per tile) and the
+// expert's tokens are the N operand (16..MAX_N), so a tile streams a 128-row
+// weight slice exactly once no matter how few tokens the expert received —
+// the low-tokens-per-expert (memory-bound) regime the layered-prefill paper
+// is about. Work items, in the order they are handed out:
+//   UP  (e, mt, nt): 128 gate rows + the matching 128 up rows, K = H.
+//                    Gate and up accumulate into separate TMEM column ranges
+//                    of the same lanes, so SiLU(g)*u is a per-thread epilogue.
+//   DN  (e, mt, nt): 128 rows of W2 (output features), K = I, waits until all
+//                    UP items of expert e have published their act rows.
+// Items are claimed dynamically (global atomic) by 1 CTA/SM; all UP items
+// precede all DN items, so a DN wait can only target items already claimed
+// by running CTAs (deadlock-free without co-residency guarantees).
+//
+// Warp roles (256 threads): w0 TMA producer + scheduler, w1 MMA issuer,
+// w2 TMEM allocator, w4..w7 epilogue (TMEM lanes 32*(w%4) ...).
+#pragma once
+#include <cuda_bf16.h>
+#include "ptx.cuh"
+
+namespace lp {
+
+constexpr int kExpertsThreads = 256;
+constexpr int kTileM = 128;        // weight rows per tile
+constexpr int kTileK = 64;         // bf16 elements per 128-byte swizzle row
+constexpr int kBoxRows = 32;       // token rows per B-operand TMA box
+constexpr int kRing = 4;           // scheduler ring depth
+constexpr int kMaxExperts = 256;
+constexpr uint32_t kATileBytes = kTileM * kTileK * 2;  // 16 KiB
+
+struct ExpertsParams {
+  int H, I, E;
+  const int32_t* offsets;      // [E+1] expert slot offsets
+  const int32_t* tile_prefix;  // [E+1] prefix sum of token tiles per expert
+  const int32_t* tile_rows;    // [E]   token rows per tile of expert e
+  __nv_bfloat16* act;          // [S, I]
+  __nv_bfloat16* y_perm;       // [S, H]
+  uint32_t* sched;             // [0] work counter, [1+e] UP items done for expert e
+};
+
+template <int MAX_N>
+struct ExpertsCfg {
+  static constexpr int kBBytes = MAX_N * 128;
+  static constexpr int kStageBytes = 2 * kATileBytes + kBBytes;
+  static constexpr int kStages = (MAX_N >= 256) ? 3 : (MAX_N >= 128 ? 4 : 5);
+  static constexpr int kAccStages = (4 * MAX_N <= 512) ? 2 : 1;
+  static constexpr int kAccCols = 2 * MAX_N;  // gate | up
+  static constexpr int kTmemCols = kAccStages * kAccCols < 32 ? 32 : kAccStages * kAccCols;
+  // barriers + ring + scalars + expert tables
+  static constexpr int kAuxBytes = 8 * (2 * kStages + 2 * kAccStages + 2 * kRing) + 16 * kRing + 16 +
+                                   4 * (3 * kMaxExperts + 2);
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
+};
+
+enum : int { kItemUp = 0, kItemDown = 1, kItemEnd = 2 };
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+
+template <int MAX_N>
+__global__ void __launch_bounds__(kExpertsThreads, 1)
+    k_experts(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
+              const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_act,
+              const ExpertsParams p) {
+  using C = ExpertsCfg<MAX_N>;
+  constexpr int S_ = C::kStages;
+  constexpr int A_ = C::kAccStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* aux = smem + S_ * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
+  uint64_t* empty = full + S_;
+  uint64_t* tfull = empty + S_;
+  uint64_t* tempty = tfull + A_;
+  uint64_t* sfull = tempty + A_;
+  uint64_t* sempty = sfull + kRing;
+  int4* ring = reinterpret_cast<int4*>(sempty + kRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+  int32_t* s_off = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  int32_t* s_tp = s_off + (kMaxExperts + 1);
+  int32_t* s_ts = s_tp + (kMaxExperts + 1);
+
+  const int warp = warp_idx();
+  const int lane = threadIdx.x & 31;
+  const int E = p.E;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], 2); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_w13); prefetch_tmap(&tm_w2); prefetch_tmap(&tm_xp); prefetch_tmap(&tm_act);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) { s_off[i] = p.offsets[i]; s_tp[i] = p.tile_prefix[i]; }
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_ts[i] = p.tile_rows[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int mt_up = p.I / kTileM;
+  const int mt_dn = p.H / kTileM;
+  const int total_tiles = s_tp[E];
+  const int n_up = mt_up * total_tiles;
+  const int n_items = (mt_up + mt_dn) * total_tiles;
+
+  if (warp == 0) {
+    // ===================== scheduler + TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+      const uint64_t pol_a = policy_evict_last();   // activations: re-read by every m-tile
+      int stage = 0; uint32_t phase = 0;
+      int r = 0; uint32_t rph = 0;
+      while (true) {
+        const int it = static_cast<int>(atomicAdd(&p.sched[0], 1u));
+        int4 info;
+        int need = 0;
+        if (it >= n_items) {
+          info = make_int4(kItemEnd, 0, 0, 0);
+        } else {
+          const bool up = it < n_up;
+          const int mtc = up ? mt_up : mt_dn;
+          const int local = up ? it : it - n_up;
+          int lo = 0, hi = E;  // largest e with mtc*tp[e] <= local
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (mtc * s_tp[mid] <= local) lo = mid; else hi = mid;
+          }
+          const int e = lo;
+          const int nt_e = s_tp[e + 1] - s_tp[e];
+          const int rr = local - mtc * s_tp[e];
+          const int mt = rr / nt_e, nt = rr - mt * nt_e;
+          const int n_e = s_off[e + 1] - s_off[e];
+          const int ts = s_ts[e];
+          const int row0 = s_off[e] + nt * ts;
+          const int nvalid = min(ts, n_e - nt * ts);
+          info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * kTileM, row0, nvalid);
+          need = mt_up * nt_e;
+        }
+        mbar_wait(&sempty[r], rph ^ 1);
+        ring[r] = info;
+        mbar_arrive(&sfull[r]);
+        if (++r == kRing) { r = 0; rph ^= 1; }
+        const int kind = info.x & 0xff;
+        if (kind == kItemEnd) break;
+        const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
+        const int nbox = (nvalid + kBoxRows - 1) / kBoxRows;
+        if (kind == kItemDown) {
+          while (ld_acquire_u32(&p.sched[1 + e]) < static_cast<uint32_t>(need)) __nanosleep(64);
+          fence_proxy_async_global();
+        }
+        const bool up = kind == kItemUp;
+        const int kblocks = up ? p.H / kTileK : p.I / kTileK;
+        const uint32_t bytes = (up ? 2 : 1) * kATileBytes + nbox * kBoxRows * 128;
+        const int arow = up ? e * 2 * p.I + m0 : e * p.H + m0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          if (up) {
+            tma_load_2d(sa, &tm_w13, &full[stage], kb * kTileK, arow, pol_w);
+            tma_load_2d(sa + kATileBytes, &tm_w13, &full[stage], kb * kTileK, arow + p.I, pol_w);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sa + 2 * kATileBytes + b * kBoxRows * 128, &tm_xp, &full[stage], kb * kTileK,
+                          row0 + b * kBoxRows, pol_a);
+          } else {
+            tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, arow, pol_w);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sa + 2 * kATileBytes + b * kBoxRows * 128, &tm_act, &full[stage], kb * kTileK,
+                          row0 + b * kBoxRows, pol_a);
+          }
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (single thread) =====================
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      int r = 0; uint32_t rph = 0;
+      int acc = 0; uint32_t aph = 0;
+      while (true) {
+        mbar_wait(&sfull[r], rph);
+        const int4 info = ring[r];
+        mbar_arrive(&sempty[r]);
+        if (++r == kRing) { r = 0; rph ^= 1; }
+        const int kind = info.x & 0xff;
+        if (kind == kItemEnd) break;
+        const bool up = kind == kItemUp;
+        const int nmma = (info.w + 15) & ~15;
+        const uint32_t idesc = idesc_bf16_f32(kTileM, nmma);
+        const int kblocks = up ? p.H / kTileK : p.I / kTileK;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_gate = tmem_base + acc * C::kAccCols;
+        const uint32_t d_up = d_gate + MAX_N;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+          const uint64_t a0 = sdesc_kmajor_sw128(sa);
+          const uint64_t a1 = sdesc_kmajor_sw128(sa + kATileBytes);
+          const uint64_t b0 = sdesc_kmajor_sw128(sa + 2 * kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kTileK / 16; ++k) {
+            const uint32_t accum = (kb | k) != 0;
+            mma_bf16(d_gate, a0 + 2 * k, b0 + 2 * k, idesc, accum);
+            if (up) mma_bf16(d_up, a1 + 2 * k, b0 + 2 * k, idesc, accum);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == A_) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> regs -> global =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = threadIdx.x - 128;
+    int r = 0; uint32_t rph = 0;
+    int acc = 0; uint32_t aph = 0;
+    while (true) {
+      mbar_wait(&sfull[r], rph);
+      const int4 info = ring[r];
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_gate = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::kAccCols;
+      const int feat = m0 + 32 * q + lane;  // output feature owned by this thread
+      const int nchunks = (nvalid + 15) / 16;
+      if (kind == kItemUp) {
+        __nv_bfloat16* dst = p.act + static_cast<size_t>(row0) * p.I + feat;
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t g[16], u[16];
+          tmem_ld16(t_gate + c * 16, g);
+          tmem_ld16(t_gate + MAX_N + c * 16, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = c * 16 + i;
+            if (n < nvalid)
+              dst[static_cast<size_t>(n) * p.I] =
+                  __float2bfloat16_rn(silu_mul(__uint_as_float(g[i]), __uint_as_float(u[i])));
+          }
+        }
+      } else {
+        __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t v[16];
+          tmem_ld16(t_gate + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = c * 16 + i;
+            if (n < nvalid) dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == A_) { acc = 0; aph ^= 1; }
+      if (kind == kItemUp) {
+        fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
+        __threadfence();
+      }
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        mbar_arrive(&sempty[r]);
+        if (kind == kItemUp) atomicAdd(&p.sched[1 + e], 1u);
+      }
+      if (++r == kRing) { r = 0; rph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+}  // namespace lp

@@ -1,0 +1,448 @@
+// liblpmoe.so — C ABI (include/lpmoe.h) over the sm_100a kernels.
+// Host side: argument validation, workspace carving, TMA descriptor encoding
+// (driver entry point, no -lcuda), launch configuration. No allocation, no
+// host synchronisation: every entry point is stream-ordered and graph-safe.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/lpmoe.h"
+#include "experts_sm100.cuh"
+#include "permute.cuh"
+#include "route.cuh"
+#include "union_counts.cuh"
+
+namespace {
+
+thread_local int g_code = LP_OK;
+thread_local cudaEvent_t g_prof[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+thread_local int g_prof_n = 0;
+
+inline void prof_mark(int i, cudaStream_t st) {
+  if (g_prof_n >= 5) cudaEventRecord(g_prof[i], st);
+}
+thread_local char g_msg[512] = "ok";
+
+int fail(int code, const char* fmt, ...) {
+  g_code = code;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_msg, sizeof(g_msg), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int ok() {
+  g_code = LP_OK;
+  return LP_OK;
+}
+#define LP_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) return fail(LP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define LP_CHECK_LAUNCH(name)                                                                       \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess) return fail(LP_ECUDA, "launch %s: %s", name, cudaGetErrorString(e_));    \
+  } while (0)
+
+constexpr int kTargetCtas = 148;  // B200 SM count; fixes ksplit independent of the device queried
+constexpr size_t kAlign = 256;
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ shapes
+int router_ksplit(int T, int H, int E) {
+  const int kb_total = H / 64;
+  const int base = ((T + lp::kRouterN - 1) / lp::kRouterN) * ((E + 127) / 128);
+  int ks = kTargetCtas / (base > 0 ? base : 1);
+  if (ks < 1) ks = 1;
+  if (ks > kb_total) ks = kb_total;
+  while (kb_total % ks) --ks;  // slices of equal K length
+  return ks;
+}
+
+int pick_max_n(int S, int E) {
+  const int avg = (S + E - 1) / E;
+  if (avg <= 40) return 64;
+  if (avg <= 96) return 128;
+  return 256;
+}
+
+struct Layout {
+  size_t partial, chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
+  size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
+  int ksplit, nchunks;
+};
+
+Layout make_layout(int T, int H, int I, int E, int topk) {
+  Layout L{};
+  const size_t S = static_cast<size_t>(T) * topk;
+  L.ksplit = router_ksplit(T, H, E);
+  L.nchunks = static_cast<int>((S + lp::kChunk - 1) / lp::kChunk);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, kAlign);
+    return at;
+  };
+  L.partial = take(static_cast<size_t>(L.ksplit) * T * E * 4);
+  L.chunk_hist = take(static_cast<size_t>(L.nchunks) * E * 4);
+  L.rank_local = take(S * 4);
+  L.ids = take(S * 4);
+  L.w = take(S * 4);
+  L.counts = take(static_cast<size_t>(E) * 4);
+  L.offsets = take(static_cast<size_t>(E + 1) * 4);
+  L.slot_of = take(S * 4);
+  L.tok_of = take(S * 4);
+  L.tile_prefix = take(static_cast<size_t>(E + 1) * 4);
+  L.tile_rows = take(static_cast<size_t>(E) * 4);
+  L.sched = take(static_cast<size_t>(E + 1) * 4);
+  L.x_perm = take(S * H * 2);
+  L.act = take(S * I * 2);
+  L.y_perm = take(S * H * 2);
+  L.total = o;
+  return L;
+}
+
+int check_dims(int T, int H, int I, int E, int topk) {
+  if (T < 0) return fail(LP_EINVAL, "T must be >= 0, got %d", T);
+  if (H <= 0 || H % 128) return fail(LP_EINVAL, "H must be a positive multiple of 128, got %d", H);
+  if (I <= 0 || I % 128) return fail(LP_EINVAL, "I must be a positive multiple of 128, got %d", I);
+  if (E < 1) return fail(LP_EINVAL, "E must be >= 1, got %d", E);
+  if (E > lp::kMaxExperts) return fail(LP_EUNSUPPORTED, "E > %d not supported, got %d", lp::kMaxExperts, E);
+  if (topk < 1 || topk > E) return fail(LP_EINVAL, "topk out of range: need 1 <= topk <= E, got %d", topk);
+  if (topk > 32) return fail(LP_EUNSUPPORTED, "topk > 32 not supported, got %d", topk);
+  return LP_OK;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(LP_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  return LP_OK;
+}
+
+// bf16 matrix [rows, cols] row-major, box = 64 cols (128 B, SWIZZLE_128B) x box_rows.
+int make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(LP_ECUDA, "cuTensorMapEncodeTiled(rows=%llu cols=%llu box_rows=%u) failed: %d",
+                (unsigned long long)rows, (unsigned long long)cols, box_rows, (int)r);
+  return LP_OK;
+}
+
+// ------------------------------------------------------------------ device info
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kTargetCtas;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return kTargetCtas;
+  return n;
+}
+
+template <typename K>
+int set_smem(K kernel, int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(LP_ECUDA, "cudaFuncSetAttribute(smem=%d): %s", bytes, cudaGetErrorString(e));
+  return LP_OK;
+}
+
+// ------------------------------------------------------------------ stages
+int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
+                 float* partial, int ksplit, cudaStream_t st) {
+  int rc;
+  if ((rc = get_encode())) return rc;
+  CUtensorMap tm_wr, tm_x;
+  if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
+  if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
+  lp::RouterParams rp{T, H, E, ksplit, (H / 64) / ksplit, (E + 127) / 128, partial};
+  if ((rc = set_smem(lp::k_router_logits, lp::kRouterSmem))) return rc;
+  const int grid = ((T + lp::kRouterN - 1) / lp::kRouterN) * rp.mtiles * ksplit;
+  lp::k_router_logits<<<grid, lp::kRouterThreads, lp::kRouterSmem, st>>>(tm_wr, tm_x, rp);
+  LP_CHECK_LAUNCH("k_router_logits");
+  const int epl = (E + 31) / 32;
+  const int tgrid = (T + 7) / 8;
+  switch (epl) {
+    case 1: lp::k_topk<1><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
+    case 2: lp::k_topk<2><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
+    case 3:
+    case 4: lp::k_topk<4><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
+    default: lp::k_topk<8><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
+  }
+  LP_CHECK_LAUNCH("k_topk");
+  return LP_OK;
+}
+
+int launch_permute(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
+                   int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
+                   int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows, uint32_t* sched,
+                   cudaStream_t st) {
+  const int S = T * topk;
+  const int nchunks = (S + lp::kChunk - 1) / lp::kChunk;
+  lp::k_chunk_hist<<<(nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
+                     lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, S, E, chunk_hist, rank_local);
+  LP_CHECK_LAUNCH("k_chunk_hist");
+  const int sb = (E + 31) / 32 * 32;
+  lp::k_scan<<<1, sb, 2 * sb * sizeof(int32_t), st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix,
+                                                       tile_rows, sched);
+  LP_CHECK_LAUNCH("k_scan");
+  lp::k_scatter<<<(S + 7) / 8, 256, 0, st>>>(ids, chunk_hist, rank_local, offsets,
+                                             static_cast<const __nv_bfloat16*>(x), S, E, topk, H, slot_of, tok_of,
+                                             static_cast<__nv_bfloat16*>(x_perm));
+  LP_CHECK_LAUNCH("k_scatter");
+  return LP_OK;
+}
+
+template <int MAX_N>
+int launch_experts_t(const void* x_perm, const void* act_in, int S, const void* w13, const void* w2, int H, int I,
+                     int E, const lp::ExpertsParams& p, cudaStream_t st) {
+  int rc;
+  if ((rc = get_encode())) return rc;
+  CUtensorMap tm_w13, tm_w2, tm_xp, tm_act;
+  if ((rc = make_tmap(&tm_w13, w13, static_cast<uint64_t>(E) * 2 * I, H, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_xp, x_perm, S, H, lp::kBoxRows))) return rc;
+  if ((rc = make_tmap(&tm_act, act_in, S, I, lp::kBoxRows))) return rc;
+  constexpr int smem = lp::ExpertsCfg<MAX_N>::kSmemBytes;
+  if ((rc = set_smem(lp::k_experts<MAX_N>, smem))) return rc;
+  lp::k_experts<MAX_N><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xp, tm_act, p);
+  LP_CHECK_LAUNCH("k_experts");
+  return LP_OK;
+}
+
+int launch_experts(const void* x_perm, int S, const void* w13, const void* w2, int H, int I, int E, int max_n,
+                   const int32_t* offsets, const int32_t* tile_prefix, const int32_t* tile_rows, uint32_t* sched,
+                   void* act, void* y_perm, cudaStream_t st) {
+  lp::ExpertsParams p{H, I, E, offsets, tile_prefix, tile_rows, static_cast<__nv_bfloat16*>(act),
+                      static_cast<__nv_bfloat16*>(y_perm), sched};
+  switch (max_n) {
+    case 64: return launch_experts_t<64>(x_perm, act, S, w13, w2, H, I, E, p, st);
+    case 128: return launch_experts_t<128>(x_perm, act, S, w13, w2, H, I, E, p, st);
+    default: return launch_experts_t<256>(x_perm, act, S, w13, w2, H, I, E, p, st);
+  }
+}
+
+// Tile schedule from externally supplied offsets (staged / expert-parallel use).
+__global__ void k_plan(const int32_t* __restrict__ offsets, int E, int max_n, int32_t* __restrict__ tile_prefix,
+                       int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched) {
+  extern __shared__ int32_t s_til[];
+  const int e = threadIdx.x;
+  const int n = (e < E) ? offsets[e + 1] - offsets[e] : 0;
+  const int nt = (n > 0) ? (n + max_n - 1) / max_n : 0;
+  s_til[e] = nt;
+  __syncthreads();
+  for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
+    const int a = (e >= o) ? s_til[e - o] : 0;
+    __syncthreads();
+    s_til[e] += a;
+    __syncthreads();
+  }
+  if (e < E) {
+    tile_prefix[e] = s_til[e] - nt;
+    const int per = nt ? (n + nt - 1) / nt : 0;
+    tile_rows[e] = min(max_n, (per + 15) & ~15);
+    if (e == E - 1) tile_prefix[E] = s_til[e];
+  }
+  for (int i = e; i <= E; i += blockDim.x) sched[i] = 0u;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* lp_version(void) { return "lpmoe 0.1 sm_100a"; }
+
+int lp_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    strncpy(buf, g_msg, n - 1);
+    buf[n - 1] = '\0';
+  }
+  return g_code;
+}
+
+size_t lp_moe_workspace_bytes(int T, int H, int I, int E, int topk) {
+  if (T < 0 || H <= 0 || I <= 0 || E <= 0 || topk <= 0) return 0;
+  return make_layout(T, H, I, E, topk).total;
+}
+
+int lp_moe_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
+                 void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dims(T, H, 128, E, topk))) return rc;
+  if (T == 0) return ok();
+  if (!x || !wr || !ids || !w || !ws) return fail(LP_EINVAL, "lp_moe_route: null pointer argument");
+  if (!aligned16(x) || !aligned16(wr)) return fail(LP_EINVAL, "lp_moe_route: x/wr must be 16-byte aligned");
+  const Layout L = make_layout(T, H, 128, E, topk);
+  const size_t need = L.partial + static_cast<size_t>(L.ksplit) * T * E * 4;
+  if (ws_bytes < need) return fail(LP_EINVAL, "lp_moe_route: workspace %zu < %zu bytes", ws_bytes, need);
+  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, at<float>(ws, L.partial), L.ksplit,
+                         static_cast<cudaStream_t>(stream))))
+    return rc;
+  return ok();
+}
+
+int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
+                   int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, void* ws, size_t ws_bytes,
+                   void* stream) {
+  int rc;
+  if ((rc = check_dims(T, H, 128, E, topk))) return rc;
+  if (!ids || !counts || !offsets || !slot_of || !tok_of || !ws || (x_perm && !x))
+    return fail(LP_EINVAL, "lp_moe_permute: null pointer argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (T == 0) {
+    LP_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st));
+    LP_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), st));
+    return ok();
+  }
+  const Layout L = make_layout(T, H, 128, E, topk);
+  if (ws_bytes < L.sched + static_cast<size_t>(E + 1) * 4)
+    return fail(LP_EINVAL, "lp_moe_permute: workspace %zu too small", ws_bytes);
+  const int max_n = pick_max_n(T * topk, E);
+  if ((rc = launch_permute(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm,
+                           at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
+                           at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched),
+                           st)))
+    return rc;
+  return ok();
+}
+
+int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void* w13, const void* w2, int H, int I,
+                   int E, void* act, void* y_perm, void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dims(0, H, I, E, 1))) return rc;
+  if (S < 0) return fail(LP_EINVAL, "S must be >= 0, got %d", S);
+  if (S == 0) return ok();
+  if (!x_perm || !offsets || !w13 || !w2 || !act || !y_perm || !ws)
+    return fail(LP_EINVAL, "lp_moe_experts: null pointer argument");
+  if (!aligned16(x_perm) || !aligned16(w13) || !aligned16(w2) || !aligned16(act) || !aligned16(y_perm))
+    return fail(LP_EINVAL, "lp_moe_experts: tensors must be 16-byte aligned");
+  const size_t need = 3 * align_up(static_cast<size_t>(E + 1) * 4, kAlign);
+  if (ws_bytes < need) return fail(LP_EINVAL, "lp_moe_experts: workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t blk = align_up(static_cast<size_t>(E + 1) * 4, kAlign);
+  int32_t* tile_prefix = at<int32_t>(ws, 0);
+  int32_t* tile_rows = at<int32_t>(ws, blk);
+  uint32_t* sched = at<uint32_t>(ws, 2 * blk);
+  const int max_n = pick_max_n(S, E);
+  const int sb = (E + 31) / 32 * 32;
+  k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
+  LP_CHECK_LAUNCH("k_plan");
+  if ((rc = launch_experts(x_perm, S, w13, w2, H, I, E, max_n, offsets, tile_prefix, tile_rows, sched, act, y_perm,
+                           st)))
+    return rc;
+  return ok();
+}
+
+int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, int T, int H, int topk, void* y,
+                   void* stream) {
+  if (T < 0 || H <= 0 || H % 8 || topk < 1) return fail(LP_EINVAL, "lp_moe_combine: bad shape T=%d H=%d topk=%d", T, H, topk);
+  if (T == 0) return ok();
+  if (!y_perm || !slot_of || !w || !y) return fail(LP_EINVAL, "lp_moe_combine: null pointer argument");
+  lp::k_combine<<<(T + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(y_perm), slot_of, w, T, topk, H, static_cast<__nv_bfloat16*>(y));
+  LP_CHECK_LAUNCH("k_combine");
+  return ok();
+}
+
+int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w2, int T, int H, int I, int E,
+                   int topk, int renorm, void* y, int32_t* ids, float* w, int32_t* counts, void* ws, size_t ws_bytes,
+                   void* stream) {
+  int rc;
+  if ((rc = check_dims(T, H, I, E, topk))) return rc;
+  if (T == 0) return ok();
+  if (!x || !wr || !w13 || !w2 || !y || !ws) return fail(LP_EINVAL, "lp_moe_forward: null pointer argument");
+  if (!aligned16(x) || !aligned16(wr) || !aligned16(w13) || !aligned16(w2) || !aligned16(y) || !aligned16(ws))
+    return fail(LP_EINVAL, "lp_moe_forward: tensors and workspace must be 16-byte aligned");
+  const Layout L = make_layout(T, H, I, E, topk);
+  if (ws_bytes < L.total) return fail(LP_EINVAL, "lp_moe_forward: workspace %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!ids) ids = at<int32_t>(ws, L.ids);
+  if (!w) w = at<float>(ws, L.w);
+  if (!counts) counts = at<int32_t>(ws, L.counts);
+  const int S = T * topk;
+  const int max_n = pick_max_n(S, E);
+  int32_t* offsets = at<int32_t>(ws, L.offsets);
+  int32_t* slot_of = at<int32_t>(ws, L.slot_of);
+  prof_mark(0, st);
+  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, at<float>(ws, L.partial), L.ksplit, st))) return rc;
+  prof_mark(1, st);
+  if ((rc = launch_permute(ids, x, T, H, E, topk, counts, offsets, slot_of, at<int32_t>(ws, L.tok_of),
+                           at<void>(ws, L.x_perm), at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local),
+                           max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                           at<uint32_t>(ws, L.sched), st)))
+    return rc;
+  prof_mark(2, st);
+  if ((rc = launch_experts(at<void>(ws, L.x_perm), S, w13, w2, H, I, E, max_n, offsets, at<int32_t>(ws, L.tile_prefix),
+                           at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
+                           at<void>(ws, L.y_perm), st)))
+    return rc;
+  prof_mark(3, st);
+  if ((rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;
+  prof_mark(4, st);
+  return ok();
+}
+
+int lp_union_counts_uniform(const double* u, int trials, int batch, int k, int E, int64_t* out, void* stream) {
+  if (trials < 0 || batch < 0 || E < 1 || E > 1024 || k < 1 || k > E)
+    return fail(LP_EINVAL, "lp_union_counts_uniform: bad shape trials=%d batch=%d k=%d E=%d", trials, batch, k, E);
+  if (k > 64) return fail(LP_EUNSUPPORTED, "lp_union_counts_uniform: k > 64 not supported");
+  if (trials == 0) return ok();
+  if (!out || (batch > 0 && !u)) return fail(LP_EINVAL, "lp_union_counts_uniform: null pointer argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t sm = ((E + 31) / 32) * sizeof(uint32_t);
+  if (k <= 16)
+    lp::k_union_uniform<16><<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, out);
+  else
+    lp::k_union_uniform<64><<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, out);
+  LP_CHECK_LAUNCH("k_union_uniform");
+  return ok();
+}
+
+int lp_union_counts_weighted(const double* u, int trials, int batch, int k, int E, const double* weights,
+                             int64_t* out, void* stream) {
+  if (trials < 0 || batch < 0 || E < 1 || E > 1024 || k < 1 || k > E)
+    return fail(LP_EINVAL, "lp_union_counts_weighted: bad shape trials=%d batch=%d k=%d E=%d", trials, batch, k, E);
+  if (trials == 0) return ok();
+  if (!out || !weights || (batch > 0 && !u)) return fail(LP_EINVAL, "lp_union_counts_weighted: null pointer argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t sm = E * sizeof(double) + ((E + 31) / 32) * sizeof(uint32_t);
+  lp::k_union_weighted<<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, weights, out);
+  LP_CHECK_LAUNCH("k_union_weighted");
+  return ok();
+}
+
+int lp_profile_events(void* const* events, int n) {
+  if (n < 0 || (n > 0 && !events)) return fail(LP_EINVAL, "lp_profile_events: bad arguments");
+  g_prof_n = n >= 5 ? 5 : 0;
+  for (int i = 0; i < 5; ++i) g_prof[i] = (g_prof_n && i < n) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+"""`GpuMoE`: the MoE layer forward over a hybrid decode+prefill batch on B200.
+
+This is the numerical layer the reference only cost-models: at the engine's
+call sites (moesim/engine.py:144-154) the simulator charges
+`moe_cost(model, routed, coverage_model.coverage(routed), layers)`
+(costmodel.py:57-85). Here `routed` tokens are actually routed and run:
+
+    y, stats = layer(x)          # x: [T, H] bf16 on cuda
+    stats.coverage               # nnz(counts)/E — what CoverageModel estimates
+    stats.expert_weight_bytes    # nnz * bytes_per_expert — moe_cost's expert_bytes
+
+Every stage is a call into liblpmoe.so through the C ABI (include/lpmoe.h);
+torch only supplies device memory and the current stream. There is no CPU or
+eager fallback: non-CUDA inputs raise.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from .types import MoEShape, ValidationError, require
+
+
+@dataclass
+class MoEStats:
+    """Routing statistics of one layer call (device tensors until read)."""
+
+    counts: torch.Tensor        # int32 [E] tokens routed to each expert
+    shape: MoEShape
+
+    @property
+    def experts_hit(self) -> int:
+        return int((self.counts > 0).sum().item())
+
+    @property
+    def coverage(self) -> float:
+        """Fraction of experts activated (the reference's coverage_fraction)."""
+        return self.experts_hit / self.shape.num_experts
+
+    @property
+    def expert_weight_bytes(self) -> int:
+        """Expert-weight HBM bytes one call streams (costmodel.py:77 with measured coverage)."""
+        return self.experts_hit * self.shape.bytes_per_expert
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_tensor(name: str, t: torch.Tensor, shape: tuple, dtype: torch.dtype) -> None:
+    require(isinstance(t, torch.Tensor), f"{name} must be a torch.Tensor")
+    require(t.is_cuda, f"{name} must be a CUDA tensor (no CPU path exists), got device {t.device}")
+    require(t.dtype == dtype, f"{name} must be {dtype}, got {t.dtype}")
+    require(tuple(t.shape) == tuple(shape), f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    require(t.is_contiguous(), f"{name} must be contiguous")
+
+
+class GpuMoE:
+    """One Qwen3-MoE-style sparse MoE block (router + E SwiGLU experts) on sm_100a.
+
+    Weights use the HF layout (transformers 5.5 modeling_qwen3_moe.py:220-224, :255):
+    wr [E,H], w13 [E,2I,H] (gate rows then up rows), w2 [E,H,I], all bf16.
+    """
+
+    def __init__(self, shape: MoEShape, wr: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor):
+        self.shape = shape
+        H, I, E = shape.hidden, shape.ffn, shape.num_experts
+        _check_tensor("wr", wr, (E, H), torch.bfloat16)
+        _check_tensor("w13", w13, (E, 2 * I, H), torch.bfloat16)
+        _check_tensor("w2", w2, (E, H, I), torch.bfloat16)
+        self.wr, self.w13, self.w2 = wr, w13, w2
+        self.device = wr.device
+        self._lib = _native.load()
+        self._ws: torch.Tensor | None = None
+        self._route_bufs: dict[int, tuple[torch.Tensor, torch.Tensor, torch.Tensor]] = {}
+
+    # ------------------------------------------------------------ workspace
+    def workspace_bytes(self, T: int) -> int:
+        s = self.shape
+        return int(self._lib.lp_moe_workspace_bytes(T, s.hidden, s.ffn, s.num_experts, s.top_k))
+
+    def workspace(self, T: int) -> torch.Tensor:
+        need = max(self.workspace_bytes(T), 256)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _bufs(self, T: int):
+        b = self._route_bufs.get(T)
+        if b is None:
+            k, E = self.shape.top_k, self.shape.num_experts
+            b = (torch.empty((T, k), dtype=torch.int32, device=self.device),
+                 torch.empty((T, k), dtype=torch.float32, device=self.device),
+                 torch.empty((E,), dtype=torch.int32, device=self.device))
+            self._route_bufs[T] = b
+        return b
+
+    # ------------------------------------------------------------ full layer
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, MoEStats]:
+        """y = MoE(x). x: [T, H] bf16 CUDA. Returns (y, stats); ids/weights in stats buffers."""
+        s = self.shape
+        require(x.dim() == 2, f"x must be 2-D [T, H], got {tuple(x.shape)}")
+        T = x.shape[0]
+        _check_tensor("x", x, (T, s.hidden), torch.bfloat16)
+        y = torch.empty_like(x) if out is None else out
+        _check_tensor("out", y, (T, s.hidden), torch.bfloat16)
+        ids, w, counts = self._bufs(T)
+        ws = self.workspace(T)
+        rc = self._lib.lp_moe_forward(
+            x.data_ptr(), self.wr.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+            T, s.hidden, s.ffn, s.num_experts, s.top_k, int(s.norm_topk_prob),
+            y.data_ptr(), ids.data_ptr(), w.data_ptr(), counts.data_ptr(),
+            ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        _native.check(rc, "lp_moe_forward")
+        self.last_ids, self.last_weights = ids, w
+        return y, MoEStats(counts, s)
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None,
+                     x_dev: torch.Tensor | None = None) -> tuple[torch.Tensor, MoEStats]:
+        """End-to-end call with host buffers: H2D copy, layer, D2H copy (stream ordered)."""
+        require(not x_host.is_cuda, "forward_host expects a host tensor")
+        xd = x_dev if x_dev is not None else torch.empty(x_host.shape, dtype=x_host.dtype, device=self.device)
+        xd.copy_(x_host, non_blocking=True)
+        yd, stats = self.forward(xd)
+        if y_host is None:
+            y_host = torch.empty(yd.shape, dtype=yd.dtype, pin_memory=True)
+        y_host.copy_(yd, non_blocking=True)
+        return y_host, stats
+
+    # ------------------------------------------------------------ staged API
+    def route(self, x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        s = self.shape
+        T = x.shape[0]
+        _check_tensor("x", x, (T, s.hidden), torch.bfloat16)
+        ids = torch.empty((T, s.top_k), dtype=torch.int32, device=self.device)
+        w = torch.empty((T, s.top_k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(T)
+        rc = self._lib.lp_moe_route(x.data_ptr(), self.wr.data_ptr(), T, s.hidden, s.num_experts, s.top_k,
+                                    int(s.norm_topk_prob), ids.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _stream_ptr(self.device))
+        _native.check(rc, "lp_moe_route")
+        return ids, w
+
+    def permute(self, ids: torch.Tensor, x: torch.Tensor | None):
+        """-> counts [E], offsets [E+1], slot_of [T*k], tok_of [T*k], x_perm [T*k, H] (or None)."""
+        s = self.shape
+        T = ids.shape[0]
+        _check_tensor("ids", ids, (T, s.top_k), torch.int32)
+        S = T * s.top_k
+        counts = torch.empty((s.num_experts,), dtype=torch.int32, device=self.device)
+        offsets = torch.empty((s.num_experts + 1,), dtype=torch.int32, device=self.device)
+        slot_of = torch.empty((S,), dtype=torch.int32, device=self.device)
+        tok_of = torch.empty((S,), dtype=torch.int32, device=self.device)
+        x_perm = None
+        if x is not None:
+            _check_tensor("x", x, (T, s.hidden), torch.bfloat16)
+            x_perm = torch.empty((S, s.hidden), dtype=torch.bfloat16, device=self.device)
+        ws = self.workspace(T)
+        rc = self._lib.lp_moe_permute(ids.data_ptr(), x.data_ptr() if x is not None else None, T, s.hidden,
+                                      s.num_experts, s.top_k, counts.data_ptr(), offsets.data_ptr(),
+                                      slot_of.data_ptr(), tok_of.data_ptr(),
+                                      x_perm.data_ptr() if x_perm is not None else None,
+                                      ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        _native.check(rc, "lp_moe_permute")
+        return counts, offsets, slot_of, tok_of, x_perm
+
+    def experts(self, x_perm: torch.Tensor, offsets: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        """-> act [S, I], y_perm [S, H] for expert-contiguous rows x_perm [S, H]."""
+        s = self.shape
+        S = x_perm.shape[0]
+        _check_tensor("x_perm", x_perm, (S, s.hidden), torch.bfloat16)
+        _check_tensor("offsets", offsets, (s.num_experts + 1,), torch.int32)
+        act = torch.empty((S, s.ffn), dtype=torch.bfloat16, device=self.device)
+        y_perm = torch.empty((S, s.hidden), dtype=torch.bfloat16, device=self.device)
+        ws = self.workspace(max(1, S // s.top_k))
+        rc = self._lib.lp_moe_experts(x_perm.data_ptr(), offsets.data_ptr(), S, self.w13.data_ptr(),
+                                      self.w2.data_ptr(), s.hidden, s.ffn, s.num_experts, act.data_ptr(),
+                                      y_perm.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        _native.check(rc, "lp_moe_experts")
+        return act, y_perm
+
+    def combine(self, y_perm: torch.Tensor, slot_of: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        s = self.shape
+        T = w.shape[0]
+        _check_tensor("w", w, (T, s.top_k), torch.float32)
+        _check_tensor("slot_of", slot_of, (T * s.top_k,), torch.int32)
+        require(y_perm.is_cuda and y_perm.dtype == torch.bfloat16 and y_perm.shape[1] == s.hidden,
+                "y_perm must be a CUDA bf16 [S, H] tensor")
+        y = torch.empty((T, s.hidden), dtype=torch.bfloat16, device=self.device)
+        rc = self._lib.lp_moe_combine(y_perm.data_ptr(), slot_of.data_ptr(), w.data_ptr(), T, s.hidden, s.top_k,
+                                      y.data_ptr(), _stream_ptr(self.device))
+        _native.check(rc, "lp_moe_combine")
+        return y
+
+
+def layer_from_seed(shape: MoEShape, seed: int, device: str = "cuda", tie_break: bool = True) -> GpuMoE:
+    """Random-init layer on the dyadic router grid (see synthetic.py)."""
+    from .synthetic import expert_weights, router_weight
+
+    wr = router_weight(shape.num_experts, shape.hidden, seed, tie_break=tie_break)
+    w13, w2 = expert_weights(shape.num_experts, shape.hidden, shape.ffn, seed + 1)
+    return GpuMoE(shape, wr.to(device), w13.to(device), w2.to(device))
