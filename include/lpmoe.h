@@ -47,7 +47,10 @@ const char* lp_version(void);
 int lp_last_error(char* buf, size_t n);
 
 /* Bytes of scratch `lp_moe_forward` needs for this shape (>= 0, 256-aligned
- * regions). Also sufficient for every staged call below. */
+ * regions). Also sufficient for every staged call below. The workspace must be
+ * zero-filled ONCE after allocation (its fixed-offset header holds the
+ * router's split-K tickets and the expert scheduler's words); every call
+ * leaves that header zeroed again, so it can be reused for any T. */
 size_t lp_moe_workspace_bytes(int T, int H, int I, int E, int topk);
 
 /* K1 — router + gating. Replaces the routing the reference only models

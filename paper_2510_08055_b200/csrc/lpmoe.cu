@@ -63,6 +63,7 @@ int router_ksplit(int T, int H, int E) {
   const int base = ((T + lp::kRouterN - 1) / lp::kRouterN) * ((E + 127) / 128);
   int ks = kTargetCtas / (base > 0 ? base : 1);
   if (ks < 1) ks = 1;
+  if (ks > lp::kRouterMaxSplit) ks = lp::kRouterMaxSplit;
   if (ks > kb_total) ks = kb_total;
   while (kb_total % ks) --ks;  // slices of equal K length
   return ks;
@@ -75,6 +76,14 @@ int pick_max_n(int S, int E) {
   return 256;
 }
 
+// Workspace header (fixed offsets, independent of T): router tickets and the
+// expert kernel's scheduler words. Must be zero-filled once after allocation;
+// every kernel leaves it zeroed again.
+constexpr int kMaxTokens = 262144;
+constexpr size_t kTicketOff = 0;
+constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB of tickets
+constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E+1 <= 257)
+
 struct Layout {
   size_t partial, chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
   size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
@@ -85,14 +94,14 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
   Layout L{};
   const size_t S = static_cast<size_t>(T) * topk;
   L.ksplit = router_ksplit(T, H, E);
-  L.nchunks = static_cast<int>((S + lp::kChunk - 1) / lp::kChunk);
-  size_t o = 0;
+  L.nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
+  size_t o = kHeaderBytes;
   auto take = [&](size_t bytes) {
     const size_t at = o;
     o = align_up(o + bytes, kAlign);
     return at;
   };
-  L.partial = take(static_cast<size_t>(L.ksplit) * T * E * 4);
+  L.partial = take(static_cast<size_t>(L.ksplit) * ((E + 127) / 128) * T * E * 4);
   L.chunk_hist = take(static_cast<size_t>(L.nchunks) * E * 4);
   L.rank_local = take(S * 4);
   L.ids = take(S * 4);
@@ -103,7 +112,7 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
   L.tok_of = take(S * 4);
   L.tile_prefix = take(static_cast<size_t>(E + 1) * 4);
   L.tile_rows = take(static_cast<size_t>(E) * 4);
-  L.sched = take(static_cast<size_t>(E + 1) * 4);
+  L.sched = kSchedOff;
   L.x_perm = take(S * H * 2);
   L.act = take(S * I * 2);
   L.y_perm = take(S * H * 2);
@@ -112,7 +121,7 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
 }
 
 int check_dims(int T, int H, int I, int E, int topk) {
-  if (T < 0) return fail(LP_EINVAL, "T must be >= 0, got %d", T);
+  if (T < 0 || T > kMaxTokens) return fail(LP_EINVAL, "T must be in [0, %d], got %d", kMaxTokens, T);
   if (H <= 0 || H % 128) return fail(LP_EINVAL, "H must be a positive multiple of 128, got %d", H);
   if (I <= 0 || I % 128) return fail(LP_EINVAL, "I must be a positive multiple of 128, got %d", I);
   if (E < 1) return fail(LP_EINVAL, "E must be >= 1, got %d", E);
@@ -170,45 +179,36 @@ int set_smem(K kernel, int bytes) {
 
 // ------------------------------------------------------------------ stages
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
-                 float* partial, int ksplit, cudaStream_t st) {
+                 void* ws, const Layout& L, cudaStream_t st) {
   int rc;
   if ((rc = get_encode())) return rc;
   CUtensorMap tm_wr, tm_x;
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
   if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
-  lp::RouterParams rp{T, H, E, ksplit, (H / 64) / ksplit, (E + 127) / 128, partial};
-  if ((rc = set_smem(lp::k_router_logits, lp::kRouterSmem))) return rc;
-  const int grid = ((T + lp::kRouterN - 1) / lp::kRouterN) * rp.mtiles * ksplit;
-  lp::k_router_logits<<<grid, lp::kRouterThreads, lp::kRouterSmem, st>>>(tm_wr, tm_x, rp);
-  LP_CHECK_LAUNCH("k_router_logits");
-  const int epl = (E + 31) / 32;
-  const int tgrid = (T + 7) / 8;
-  switch (epl) {
-    case 1: lp::k_topk<1><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
-    case 2: lp::k_topk<2><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
-    case 3:
-    case 4: lp::k_topk<4><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
-    default: lp::k_topk<8><<<tgrid, 256, 0, st>>>(partial, T, E, ksplit, topk, renorm, ids, w); break;
-  }
-  LP_CHECK_LAUNCH("k_topk");
+  char* base = static_cast<char*>(ws);
+  lp::RouterParams rp{T, H, E, topk, renorm, L.ksplit, (H / 64) / L.ksplit, (E + 127) / 128,
+                      reinterpret_cast<float*>(base + L.partial), reinterpret_cast<uint32_t*>(base + kTicketOff), ids,
+                      w, reinterpret_cast<int32_t*>(base + L.chunk_hist),
+                      reinterpret_cast<int32_t*>(base + L.rank_local)};
+  if ((rc = set_smem(lp::k_router, lp::kRouterSmem))) return rc;
+  const int grid = L.nchunks * rp.mtiles * L.ksplit;
+  lp::k_router<<<grid, lp::kRouterThreads, lp::kRouterSmem, st>>>(tm_wr, tm_x, rp);
+  LP_CHECK_LAUNCH("k_router");
   return LP_OK;
 }
 
-int launch_permute(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
-                   int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
-                   int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows, uint32_t* sched,
-                   cudaStream_t st) {
+// chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
+int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
+                        int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
+                        const int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows,
+                        uint32_t* sched, cudaStream_t st) {
   const int S = T * topk;
-  const int nchunks = (S + lp::kChunk - 1) / lp::kChunk;
-  lp::k_chunk_hist<<<(nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
-                     lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, S, E, chunk_hist, rank_local);
-  LP_CHECK_LAUNCH("k_chunk_hist");
-  const int sb = (E + 31) / 32 * 32;
-  lp::k_scan<<<1, sb, 2 * sb * sizeof(int32_t), st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix,
-                                                       tile_rows, sched);
+  const int nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
+  lp::k_scan<<<1, 1024, 0, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows, sched);
   LP_CHECK_LAUNCH("k_scan");
   lp::k_scatter<<<(S + 7) / 8, 256, 0, st>>>(ids, chunk_hist, rank_local, offsets,
-                                             static_cast<const __nv_bfloat16*>(x), S, E, topk, H, slot_of, tok_of,
+                                             static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
+                                             lp::kRouterN * topk, slot_of, tok_of,
                                              static_cast<__nv_bfloat16*>(x_perm));
   LP_CHECK_LAUNCH("k_scatter");
   return LP_OK;
@@ -300,11 +300,8 @@ int lp_moe_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   if (!x || !wr || !ids || !w || !ws) return fail(LP_EINVAL, "lp_moe_route: null pointer argument");
   if (!aligned16(x) || !aligned16(wr)) return fail(LP_EINVAL, "lp_moe_route: x/wr must be 16-byte aligned");
   const Layout L = make_layout(T, H, 128, E, topk);
-  const size_t need = L.partial + static_cast<size_t>(L.ksplit) * T * E * 4;
-  if (ws_bytes < need) return fail(LP_EINVAL, "lp_moe_route: workspace %zu < %zu bytes", ws_bytes, need);
-  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, at<float>(ws, L.partial), L.ksplit,
-                         static_cast<cudaStream_t>(stream))))
-    return rc;
+  if (ws_bytes < L.ids) return fail(LP_EINVAL, "lp_moe_route: workspace %zu < %zu bytes", ws_bytes, L.ids);
+  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, static_cast<cudaStream_t>(stream)))) return rc;
   return ok();
 }
 
@@ -322,13 +319,17 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
     return ok();
   }
   const Layout L = make_layout(T, H, 128, E, topk);
-  if (ws_bytes < L.sched + static_cast<size_t>(E + 1) * 4)
-    return fail(LP_EINVAL, "lp_moe_permute: workspace %zu too small", ws_bytes);
+  if (ws_bytes < L.x_perm) return fail(LP_EINVAL, "lp_moe_permute: workspace %zu < %zu bytes", ws_bytes, L.x_perm);
   const int max_n = pick_max_n(T * topk, E);
-  if ((rc = launch_permute(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm,
-                           at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
-                           at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched),
-                           st)))
+  int32_t* chunk_hist = at<int32_t>(ws, L.chunk_hist);
+  int32_t* rank_local = at<int32_t>(ws, L.rank_local);
+  const int chunk = lp::kRouterN * topk;
+  lp::k_chunk_hist<<<(L.nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
+                     lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, T * topk, E, chunk, chunk_hist, rank_local);
+  LP_CHECK_LAUNCH("k_chunk_hist");
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm, chunk_hist,
+                                rank_local, max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                at<uint32_t>(ws, L.sched), st)))
     return rc;
   return ok();
 }
@@ -343,13 +344,13 @@ int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void
     return fail(LP_EINVAL, "lp_moe_experts: null pointer argument");
   if (!aligned16(x_perm) || !aligned16(w13) || !aligned16(w2) || !aligned16(act) || !aligned16(y_perm))
     return fail(LP_EINVAL, "lp_moe_experts: tensors must be 16-byte aligned");
-  const size_t need = 3 * align_up(static_cast<size_t>(E + 1) * 4, kAlign);
+  const size_t blk = align_up(static_cast<size_t>(E + 1) * 4, kAlign);
+  const size_t need = kHeaderBytes + 2 * blk;
   if (ws_bytes < need) return fail(LP_EINVAL, "lp_moe_experts: workspace %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t blk = align_up(static_cast<size_t>(E + 1) * 4, kAlign);
-  int32_t* tile_prefix = at<int32_t>(ws, 0);
-  int32_t* tile_rows = at<int32_t>(ws, blk);
-  uint32_t* sched = at<uint32_t>(ws, 2 * blk);
+  int32_t* tile_prefix = at<int32_t>(ws, kHeaderBytes);
+  int32_t* tile_rows = at<int32_t>(ws, kHeaderBytes + blk);
+  uint32_t* sched = at<uint32_t>(ws, kSchedOff);
   const int max_n = pick_max_n(S, E);
   const int sb = (E + 31) / 32 * 32;
   k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
@@ -365,7 +366,8 @@ int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, i
   if (T < 0 || H <= 0 || H % 8 || topk < 1) return fail(LP_EINVAL, "lp_moe_combine: bad shape T=%d H=%d topk=%d", T, H, topk);
   if (T == 0) return ok();
   if (!y_perm || !slot_of || !w || !y) return fail(LP_EINVAL, "lp_moe_combine: null pointer argument");
-  lp::k_combine<<<(T + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  if (H / 8 > 32 * lp::kCombineThreads) return fail(LP_EUNSUPPORTED, "lp_moe_combine: H too large");
+  lp::k_combine<<<T, lp::kCombineThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(y_perm), slot_of, w, T, topk, H, static_cast<__nv_bfloat16*>(y));
   LP_CHECK_LAUNCH("k_combine");
   return ok();
@@ -391,12 +393,12 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   int32_t* offsets = at<int32_t>(ws, L.offsets);
   int32_t* slot_of = at<int32_t>(ws, L.slot_of);
   prof_mark(0, st);
-  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, at<float>(ws, L.partial), L.ksplit, st))) return rc;
+  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
   prof_mark(1, st);
-  if ((rc = launch_permute(ids, x, T, H, E, topk, counts, offsets, slot_of, at<int32_t>(ws, L.tok_of),
-                           at<void>(ws, L.x_perm), at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local),
-                           max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
-                           at<uint32_t>(ws, L.sched), st)))
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, at<int32_t>(ws, L.tok_of),
+                                at<void>(ws, L.x_perm), at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local),
+                                max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                at<uint32_t>(ws, L.sched), st)))
     return rc;
   prof_mark(2, st);
   if ((rc = launch_experts(at<void>(ws, L.x_perm), S, w13, w2, H, I, E, max_n, offsets, at<int32_t>(ws, L.tile_prefix),

@@ -18,11 +18,13 @@
 
 namespace lp {
 
-constexpr int kChunk = 512;          // routing entries per histogram warp
 constexpr int kHistWarps = 4;
 
+// Standalone permutation path (ids supplied by the caller): per tile of
+// kRouterN tokens (chunk = kRouterN*topk entries) the same stable histogram +
+// in-tile ranks the router kernel produces. One warp per tile.
 __global__ void __launch_bounds__(32 * kHistWarps)
-    k_chunk_hist(const int32_t* __restrict__ ids, int S, int E, int32_t* __restrict__ chunk_hist,
+    k_chunk_hist(const int32_t* __restrict__ ids, int S, int E, int chunk, int32_t* __restrict__ chunk_hist,
                  int32_t* __restrict__ rank_local) {
   extern __shared__ int32_t sh_hist[];
   const int wl = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -30,12 +32,12 @@ __global__ void __launch_bounds__(32 * kHistWarps)
   int32_t* hist = sh_hist + wl * E;
   for (int e = lane; e < E; e += 32) hist[e] = 0;
   __syncwarp();
-  const int nchunks = (S + kChunk - 1) / kChunk;
+  const int nchunks = (S + chunk - 1) / chunk;
   if (c < nchunks) {
     const unsigned lt = (1u << lane) - 1u;
-    for (int s = 0; s < kChunk; s += 32) {
-      const int i = c * kChunk + s + lane;
-      const int e = (i < S) ? ids[i] : -1;
+    for (int s = 0; s < chunk; s += 32) {
+      const int i = c * chunk + s + lane;
+      const int e = (s + lane < chunk && i < S) ? ids[i] : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, e);
       int base = 0;
       if (e >= 0) base = hist[e];
@@ -50,75 +52,96 @@ __global__ void __launch_bounds__(32 * kHistWarps)
   }
 }
 
-// Single block, one thread per expert (E <= blockDim.x <= 1024).
-__global__ void k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n,
-                       int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
-                       int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
-                       uint32_t* __restrict__ sched) {
-  extern __shared__ int32_t sh[];
-  int32_t* s_cnt = sh;               // [blockDim]
-  int32_t* s_til = sh + blockDim.x;  // [blockDim]
-  const int e = threadIdx.x;
-  int run = 0;
-  if (e < E) {
-    int c = 0;
-    for (; c + 4 <= nchunks; c += 4) {
-      const int v0 = chunk_hist[static_cast<size_t>(c) * E + e];
-      const int v1 = chunk_hist[static_cast<size_t>(c + 1) * E + e];
-      const int v2 = chunk_hist[static_cast<size_t>(c + 2) * E + e];
-      const int v3 = chunk_hist[static_cast<size_t>(c + 3) * E + e];
-      chunk_hist[static_cast<size_t>(c) * E + e] = run;
-      chunk_hist[static_cast<size_t>(c + 1) * E + e] = run + v0;
-      chunk_hist[static_cast<size_t>(c + 2) * E + e] = run + v0 + v1;
-      chunk_hist[static_cast<size_t>(c + 3) * E + e] = run + v0 + v1 + v2;
-      run += v0 + v1 + v2 + v3;
+// Single block of 1024 threads: G = 1024/E_pad groups of E_pad threads; group g
+// owns a contiguous range of chunks. Pass 1 sums the range, the G partial sums
+// are scanned, pass 2 rewrites chunk_hist in place as per-chunk exclusive bases
+// (fixed order). Then offsets, the expert kernel's token-tile schedule, and the
+// reset of its scheduler words.
+__global__ void __launch_bounds__(1024)
+    k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n, int32_t* __restrict__ counts,
+           int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
+           uint32_t* __restrict__ sched) {
+  __shared__ int32_t s_part[1024];
+  __shared__ int32_t s_cnt[256];
+  __shared__ int32_t s_til[256];
+  const int e_pad = (E + 31) & ~31;
+  const int G = blockDim.x / e_pad;
+  const int g = threadIdx.x / e_pad;
+  const int e = threadIdx.x % e_pad;
+  const int per = (nchunks + G - 1) / G;
+  const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
+  int sum = 0;
+  if (g < G && e < E) {
+    int c = c0;
+    for (; c + 4 <= c1; c += 4) {
+      sum += __ldcg(chunk_hist + static_cast<size_t>(c) * E + e) + __ldcg(chunk_hist + static_cast<size_t>(c + 1) * E + e) +
+             __ldcg(chunk_hist + static_cast<size_t>(c + 2) * E + e) + __ldcg(chunk_hist + static_cast<size_t>(c + 3) * E + e);
     }
-    for (; c < nchunks; ++c) {
-      const int v = chunk_hist[static_cast<size_t>(c) * E + e];
-      chunk_hist[static_cast<size_t>(c) * E + e] = run;
+    for (; c < c1; ++c) sum += __ldcg(chunk_hist + static_cast<size_t>(c) * E + e);
+  }
+  if (g < G) s_part[g * e_pad + e] = sum;
+  __syncthreads();
+  if (threadIdx.x < e_pad) {
+    int run = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      const int v = s_part[gg * e_pad + threadIdx.x];
+      s_part[gg * e_pad + threadIdx.x] = run;
       run += v;
     }
-    counts[e] = run;
+    s_cnt[threadIdx.x] = (threadIdx.x < E) ? run : 0;
   }
-  const int ntiles = (e < E && run > 0) ? (run + max_n - 1) / max_n : 0;
-  s_cnt[e] = (e < E) ? run : 0;
-  s_til[e] = ntiles;
   __syncthreads();
-  // Hillis-Steele inclusive scans (E <= 1024, negligible)
-  for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
-    const int a = (e >= o) ? s_cnt[e - o] : 0;
-    const int b = (e >= o) ? s_til[e - o] : 0;
-    __syncthreads();
-    s_cnt[e] += a;
-    s_til[e] += b;
-    __syncthreads();
-  }
-  if (e < E) {
-    offsets[e] = s_cnt[e] - run;
-    tile_prefix[e] = s_til[e] - ntiles;
-    // even split of the expert's rows over its tiles, rounded to the MMA N step
-    const int per = ntiles ? (run + ntiles - 1) / ntiles : 0;
-    tile_rows[e] = min(max_n, (per + 15) & ~15);
-    if (e == E - 1) {
-      offsets[E] = s_cnt[e];
-      tile_prefix[E] = s_til[e];
+  if (g < G && e < E) {
+    int run = s_part[g * e_pad + e];
+    for (int c = c0; c < c1; ++c) {
+      const size_t at = static_cast<size_t>(c) * E + e;
+      const int v = __ldcg(chunk_hist + at);
+      chunk_hist[at] = run;
+      run += v;
     }
   }
-  for (int i = e; i <= E; i += blockDim.x) sched[i] = 0u;
+  // offsets / tile schedule over experts (e_pad <= 256 threads)
+  const int me = threadIdx.x;
+  int cnt = 0, ntiles = 0;
+  if (me < e_pad) {
+    cnt = s_cnt[me];
+    ntiles = (cnt > 0) ? (cnt + max_n - 1) / max_n : 0;
+    s_til[me] = ntiles;
+    if (me < E) counts[me] = cnt;
+  }
+  __syncthreads();
+  for (int o = 1; o < e_pad; o <<= 1) {
+    int a = 0, b = 0;
+    if (me < e_pad && me >= o) { a = s_cnt[me - o]; b = s_til[me - o]; }
+    __syncthreads();
+    if (me < e_pad) { s_cnt[me] += a; s_til[me] += b; }
+    __syncthreads();
+  }
+  if (me < E) {
+    offsets[me] = s_cnt[me] - cnt;
+    tile_prefix[me] = s_til[me] - ntiles;
+    const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
+    tile_rows[me] = min(max_n, (rows + 15) & ~15);
+    if (me == E - 1) {
+      offsets[E] = s_cnt[me];
+      tile_prefix[E] = s_til[me];
+    }
+  }
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) sched[i] = 0u;
 }
 
 // One warp per routing entry: final slot, inverse map, and the row gather.
 __global__ void __launch_bounds__(256)
     k_scatter(const int32_t* __restrict__ ids, const int32_t* __restrict__ chunk_base,
               const int32_t* __restrict__ rank_local, const int32_t* __restrict__ offsets,
-              const __nv_bfloat16* __restrict__ x, int S, int E, int topk, int H,
+              const __nv_bfloat16* __restrict__ x, int S, int E, int topk, int H, int chunk,
               int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of, __nv_bfloat16* __restrict__ x_perm) {
   const int i = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (i >= S) return;
   const int e = ids[i];
   const int t = i / topk;
-  const int slot = offsets[e] + chunk_base[static_cast<size_t>(i / kChunk) * E + e] + rank_local[i];
+  const int slot = offsets[e] + chunk_base[static_cast<size_t>(i / chunk) * E + e] + rank_local[i];
   if (lane == 0) {
     slot_of[i] = slot;
     tok_of[slot] = t;
@@ -131,50 +154,60 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]]   (fp32 accumulate, bf16 out)
-__global__ void __launch_bounds__(256)
+// y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]]   (fp32 accumulate in fixed j order, bf16 out)
+// One CTA per token; each thread owns 8 consecutive features and keeps all
+// topk row loads in flight.
+constexpr int kCombineThreads = 256;
+__global__ void __launch_bounds__(kCombineThreads)
     k_combine(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __restrict__ slot_of,
               const float* __restrict__ w, int T, int topk, int H, __nv_bfloat16* __restrict__ y) {
-  const int t = blockIdx.x * 8 + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
+  __shared__ int s_slot[32];
+  __shared__ float s_w[32];
+  const int t = blockIdx.x;
+  if (threadIdx.x < topk) {
+    s_slot[threadIdx.x] = slot_of[static_cast<size_t>(t) * topk + threadIdx.x];
+    s_w[threadIdx.x] = w[static_cast<size_t>(t) * topk + threadIdx.x];
+  }
+  __syncthreads();
   const int nv = H / 8;
-  for (int v0 = 0; v0 < nv; v0 += 32 * 4) {
-    float acc[4][8];
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    float acc[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    int j = 0;
+    for (; j + 4 <= topk; j += 4) {
+      uint4 d[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
-    for (int j = 0; j < topk; ++j) {
-      const int slot = slot_of[static_cast<size_t>(t) * topk + j];
-      const float wj = w[static_cast<size_t>(t) * topk + j];
-      const uint4* src = reinterpret_cast<const uint4*>(y_perm + static_cast<size_t>(slot) * H);
+      for (int u = 0; u < 4; ++u)
+        d[u] = __ldcg(reinterpret_cast<const uint4*>(y_perm + static_cast<size_t>(s_slot[j + u]) * H) + v);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int v = v0 + u * 32 + lane;
-        if (v < nv) {
-          const uint4 d = src[v];
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d[u]);
+        const float wj = s_w[j + u];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f = __bfloat1622float2(h2[q]);
-            acc[u][2 * q] += wj * f.x;
-            acc[u][2 * q + 1] += wj * f.y;
-          }
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(h2[q]);
+          acc[2 * q] += wj * f.x;
+          acc[2 * q + 1] += wj * f.y;
         }
       }
     }
+    for (; j < topk; ++j) {
+      const uint4 d = __ldcg(reinterpret_cast<const uint4*>(y_perm + static_cast<size_t>(s_slot[j]) * H) + v);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d);
+      const float wj = s_w[j];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int v = v0 + u * 32 + lane;
-      if (v < nv) {
-        uint4 o;
-        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) o2[q] = __floats2bfloat162_rn(acc[u][2 * q], acc[u][2 * q + 1]);
-        reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * H)[v] = o;
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h2[q]);
+        acc[2 * q] += wj * f.x;
+        acc[2 * q + 1] += wj * f.y;
       }
     }
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o2[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+    reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * H)[v] = o;
   }
 }
 

@@ -1,57 +1,73 @@
-// K1: router logits (tcgen05) + softmax/top-k gating (warp shuffles).
+// K1: router logits (tcgen05) + softmax / top-k gating + per-tile expert
+// histogram, in ONE launch.
 //
 // Semantics follow HF transformers 5.5 `Qwen3MoeTopKRouter.forward`
 // (modeling_qwen3_moe.py:260-270): logits = x . Wr^T accumulated in fp32,
 // softmax over all E experts in fp32, top-k, optional renormalisation of the
 // k selected probabilities (`norm_topk_prob`). Tie-break is fixed as
-// (probability desc, expert index asc) on both the GPU and the oracle.
+// (logit desc, expert index asc) on both the GPU and the oracle.
 //
-// The logits GEMM is swap-AB like the expert kernel: M = 128 expert rows of Wr,
-// N = RN tokens, split along H into `ksplit` slices so small token counts still
-// fill the machine; partial sums are reduced in a fixed order by the top-k
-// kernel, so the result is deterministic run to run.
+// Tiling: M = 128 expert rows of Wr (E <= 256 -> up to 2 m-tiles), N = 32
+// tokens per tile, K = H split into `ksplit` equal slices so small batches
+// still spread over the SMs. Every (tile, m-tile, split) CTA stores its fp32
+// partial logits; the LAST CTA to arrive for a token tile (global ticket,
+// self-resetting) sums the partials in fixed split order — deterministic run
+// to run — and then, with its four epilogue warps:
+//   * softmax + top-k per token (warp shuffles), writes ids / weights;
+//   * stable per-tile expert histogram + in-tile ranks of the routing entries
+//     (match_any within a warp, exclusive scan across the 4 warps), which the
+//     permutation (permute.cuh) turns into expert-contiguous slots.
 #pragma once
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 
 namespace lp {
 
-constexpr int kRouterN = 64;       // tokens per router tile
+constexpr int kRouterN = 32;        // tokens per router tile (= permutation chunk)
 constexpr int kRouterStages = 4;
-constexpr int kRouterThreads = 192;
-constexpr int kRouterSmem = 1024 + kRouterStages * (16384 + kRouterN * 128) + 256;
+constexpr int kRouterThreads = 192; // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
+constexpr int kRouterMaxSplit = 8;
+constexpr int kRouterStage = 16384 + kRouterN * 128;
+constexpr int kRouterSmem = 1024 + kRouterStages * kRouterStage + 256;
 
 struct RouterParams {
-  int T, H, E;
-  int ksplit;     // number of H slices
-  int kb_split;   // 64-wide K blocks per slice
-  int mtiles;     // ceil(E / 128)
-  float* partial; // [ksplit, T, E]
+  int T, H, E, topk, renorm;
+  int ksplit;        // number of H slices
+  int kb_split;      // 64-wide K blocks per slice
+  int mtiles;        // ceil(E / 128)
+  float* partial;    // [ksplit * mtiles, T, E] (unused when ksplit*mtiles == 1)
+  uint32_t* ticket;  // [ntiles], zero between calls (self-resetting)
+  int32_t* ids;      // [T, topk]
+  float* w;          // [T, topk]
+  int32_t* tile_hist;   // [ntiles, E] per-tile expert counts
+  int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its tile
 };
 
 __global__ void __launch_bounds__(kRouterThreads, 1)
-    k_router_logits(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
-                    const RouterParams p) {
+    k_router(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
+             const RouterParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kStage = 16384 + kRouterN * 128;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStages * kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStages * kRouterStage);
   uint64_t* empty = full + kRouterStages;
   uint64_t* tfull = empty + kRouterStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
+  const int arrivals = p.ksplit * p.mtiles;
   const int split = blockIdx.x % p.ksplit;
   const int mt = (blockIdx.x / p.ksplit) % p.mtiles;
-  const int nt = blockIdx.x / (p.ksplit * p.mtiles);
+  const int nt = blockIdx.x / arrivals;
+  const int t0 = nt * kRouterN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRouterStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kRouterN);
+  if (warp == 1) tmem_alloc(tmem_slot, 32);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -64,10 +80,10 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       for (int i = 0; i < p.kb_split; ++i) {
         const int s = i % kRouterStages;
         mbar_wait(&empty[s], ((i / kRouterStages) & 1) ^ 1);
-        uint8_t* sa = smem + s * kStage;
-        mbar_arrive_expect_tx(&full[s], kStage);
+        uint8_t* sa = smem + s * kRouterStage;
+        mbar_arrive_expect_tx(&full[s], kRouterStage);
         tma_load_2d(sa, &tm_wr, &full[s], (kb0 + i) * 64, mt * 128, pol);
-        tma_load_2d(sa + 16384, &tm_x, &full[s], (kb0 + i) * 64, nt * kRouterN, pol);
+        tma_load_2d(sa + 16384, &tm_x, &full[s], (kb0 + i) * 64, t0, pol);
       }
     }
   } else if (warp == 1) {
@@ -77,7 +93,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         const int s = i % kRouterStages;
         mbar_wait(&full[s], (i / kRouterStages) & 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * kStage);
+        const uint32_t sa = smem_u32(smem + s * kRouterStage);
         const uint64_t a = sdesc_kmajor_sw128(sa);
         const uint64_t b = sdesc_kmajor_sw128(sa + 16384);
 #pragma unroll
@@ -87,21 +103,160 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       mma_commit(tfull);
     }
   } else {
+    // ========================= epilogue: 4 warps, 128 threads =========================
     const int q = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    const int e_pad = (p.E + 31) & ~31;
+    float* s_logit = reinterpret_cast<float*>(smem);  // [kRouterN][e_pad], pipeline smem is free now
+    int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][topk]
+    int32_t* s_wh = s_ids + kRouterN * 32;                                 // [4][e_pad] warp histograms
     mbar_wait(tfull, 0);
     tc_fence_after();
     const int e = mt * 128 + 32 * q + lane;
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
-#pragma unroll 1
-    for (int c = 0; c < kRouterN / 16; ++c) {
-      uint32_t v[16];
-      tmem_ld16(taddr + c * 16, v);
+    uint32_t v[32];
+    {
+      uint32_t a[16], b[16];
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+      tmem_ld16(taddr, a);
+      tmem_ld16(taddr + 16, b);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int t = nt * kRouterN + c * 16 + i;
-        if (t < p.T && e < p.E)
-          p.partial[(static_cast<size_t>(split) * p.T + t) * p.E + e] = __uint_as_float(v[i]);
+      for (int i = 0; i < 16; ++i) { v[i] = a[i]; v[16 + i] = b[i]; }
+    }
+    bool last = true;
+    if (arrivals > 1) {
+      const int slice = split * p.mtiles + mt;
+      float* dst = p.partial + (static_cast<size_t>(slice) * p.T) * p.E;
+#pragma unroll
+      for (int i = 0; i < kRouterN; ++i) {
+        const int t = t0 + i;
+        if (t < p.T && e < p.E) dst[static_cast<size_t>(t) * p.E + e] = __uint_as_float(v[i]);
+      }
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        const uint32_t old = atomicAdd(&p.ticket[nt], 1u);
+        *s_flag = (old == static_cast<uint32_t>(arrivals - 1));
+      }
+      named_bar_sync(1, 128);
+      last = *s_flag != 0;
+      if (last) {
+        __threadfence();
+        if (et == 0) p.ticket[nt] = 0u;  // ready for the next call
+        // fixed-order reduction of all slices: s_logit[t][e]
+        for (int ee = et; ee < e_pad; ee += 128) {
+          for (int i = 0; i < kRouterN; ++i) {
+            const int t = t0 + i;
+            float acc = 0.f;
+            if (t < p.T && ee < p.E) {
+              const int emt = ee >> 7;
+              for (int sp = 0; sp < p.ksplit; ++sp)
+                acc += __ldcg(p.partial + (static_cast<size_t>(sp * p.mtiles + emt) * p.T + t) * p.E + ee);
+            }
+            s_logit[i * e_pad + ee] = acc;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kRouterN; ++i) s_logit[i * e_pad + e] = __uint_as_float(v[i]);
+    }
+    named_bar_sync(1, 128);
+    if (last) {
+      // ---------------- softmax + top-k: warp q owns tokens q*8 .. q*8+7 ----------------
+      const int epl = e_pad / 32;
+      for (int i = q * 8; i < q * 8 + 8; ++i) {
+        const int t = t0 + i;
+        if (t >= p.T) break;
+        float l[8];
+        float m = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int ex = lane + 32 * j;
+          l[j] = (j < epl && ex < p.E) ? s_logit[i * e_pad + ex] : -INFINITY;
+          m = fmaxf(m, l[j]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float ssum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        float psel = 0.f, psum = 0.f;
+        int my_id = 0;
+        for (int r = 0; r < p.topk; ++r) {
+          float bv = -INFINITY;
+          int bi = 0x7fffffff, bj = -1;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int ex = lane + 32 * j;
+            if (l[j] > bv || (l[j] == bv && l[j] != -INFINITY && ex < bi)) { bv = l[j]; bi = ex; bj = j; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (lane + 32 * j == bi) l[j] = -INFINITY;
+          (void)bj;
+          const float pr = expf(bv - m) / ssum;
+          psum += pr;
+          if (lane == r) { psel = pr; my_id = bi; }
+        }
+        if (lane < p.topk) {
+          p.ids[static_cast<size_t>(t) * p.topk + lane] = my_id;
+          p.w[static_cast<size_t>(t) * p.topk + lane] = p.renorm ? psel / psum : psel;
+          s_ids[i * p.topk + lane] = my_id;
+        }
+      }
+      // ---------------- stable per-tile histogram + ranks ----------------
+      for (int ee = lane; ee < e_pad; ee += 32) s_wh[q * e_pad + ee] = 0;
+      __syncwarp();
+      const int tok_lo = min(q * 8, max(p.T - t0, 0));
+      const int tok_hi = min(q * 8 + 8, p.T - t0);
+      const int n_ent = max(tok_hi - tok_lo, 0) * p.topk;
+      const unsigned lt = (1u << lane) - 1u;
+      int my_rank[8];  // ranks for this lane's entries (<= 8 steps since 8 tokens * topk <= 256)
+      int my_e[8];
+      for (int st = 0; st < 8; ++st) {
+        const int k0 = st * 32;
+        my_e[st] = -1;
+        my_rank[st] = 0;
+        if (k0 >= n_ent) continue;
+        const int idx = k0 + lane;
+        const int ex = (idx < n_ent) ? s_ids[tok_lo * p.topk + idx] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, ex);
+        int base = 0;
+        if (ex >= 0) base = s_wh[q * e_pad + ex];
+        __syncwarp();
+        if (ex >= 0) {
+          my_rank[st] = base + __popc(peers & lt);
+          my_e[st] = ex;
+          if ((__ffs(peers) - 1) == lane) s_wh[q * e_pad + ex] = base + __popc(peers);
+        }
+        __syncwarp();
+      }
+      named_bar_sync(1, 128);
+      // exclusive scan over the 4 warps per expert; tile totals to global
+      for (int ee = et; ee < e_pad; ee += 128) {
+        int run = 0;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          const int c = s_wh[w4 * e_pad + ee];
+          s_wh[w4 * e_pad + ee] = run;
+          run += c;
+        }
+        if (ee < p.E) p.tile_hist[static_cast<size_t>(nt) * p.E + ee] = run;
+      }
+      named_bar_sync(1, 128);
+      for (int st = 0; st < 8; ++st) {
+        const int idx = st * 32 + lane;
+        if (my_e[st] >= 0)
+          p.rank_local[static_cast<size_t>(t0 + tok_lo) * p.topk + idx] = my_rank[st] + s_wh[q * e_pad + my_e[st]];
       }
     }
   }
@@ -109,70 +264,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kRouterN);
-  }
-}
-
-// One warp per token. Lane l owns experts l, l+32, ... (EPL of them).
-template <int EPL>
-__global__ void __launch_bounds__(256) k_topk(const float* __restrict__ partial, int T, int E, int ksplit,
-                                              int topk, int renorm, int32_t* __restrict__ ids,
-                                              float* __restrict__ w) {
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (t >= T) return;
-  float l[EPL];
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) {
-    const int e = lane + 32 * j;
-    float acc = 0.f;
-    if (e < E) {
-      for (int s = 0; s < ksplit; ++s) acc += partial[(static_cast<size_t>(s) * T + t) * E + e];
-    }
-    l[j] = (e < E) ? acc : -INFINITY;
-  }
-  // softmax statistics over all E (fp32, like softmax(dtype=float))
-  float m = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) m = fmaxf(m, l[j]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float ssum = 0.f;
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
-
-  bool taken[EPL];
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) taken[j] = false;
-  float psel = 0.f, psum = 0.f;
-  int my_id = 0;
-  for (int r = 0; r < topk; ++r) {
-    // local best (value desc, index asc)
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int j = 0; j < EPL; ++j) {
-      const int e = lane + 32 * j;
-      if (!taken[j] && e < E && (l[j] > bv || (l[j] == bv && e < bi))) { bv = l[j]; bi = e; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-#pragma unroll
-    for (int j = 0; j < EPL; ++j)
-      if (lane + 32 * j == bi) taken[j] = true;
-    const float pr = expf(bv - m) / ssum;
-    psum += pr;
-    if (lane == r) { psel = pr; my_id = bi; }
-  }
-  if (lane < topk) {
-    ids[static_cast<size_t>(t) * topk + lane] = my_id;
-    w[static_cast<size_t>(t) * topk + lane] = renorm ? psel / psum : psel;
+    tmem_dealloc(tmem_base, 32);
   }
 }
 

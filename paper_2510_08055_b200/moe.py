@@ -85,7 +85,8 @@ class GpuMoE:
     def workspace(self, T: int) -> torch.Tensor:
         need = max(self.workspace_bytes(T), 256)
         if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            # zero-filled once: the header holds self-resetting split-K tickets (lpmoe.h)
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
     def _bufs(self, T: int):
