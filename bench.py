@@ -58,7 +58,13 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling around the timed region (B200_PROFILING.md clocks line).
+
+    Started before the warm-up so the 100 ms sampler is already running when
+    the (often only tens of ms long) timed region starts; each sample is
+    stamped with host time and summary() keeps those inside the timed window
+    (padded by one sampling period), falling back to the whole busy phase.
+    """
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -68,23 +74,25 @@ class ClockSampler:
         self.gpu = gpu_index
         self.rows = []
         self.proc = None
+        self.err = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
-        except FileNotFoundError:
+        except FileNotFoundError as exc:
+            self.err = str(exc)
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -92,16 +100,29 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
             self.th.join(timeout=2)
+            if not self.rows:
+                self.err = (self.proc.stderr.read() or "no samples")[:200]
 
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+    def summary(self, t0: float, t1: float):
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        win = [r for t, r in self.rows if t0 - 0.06 <= t <= t1 + 0.06]
+        window = "timed"
+        if not win:
+            win = [r for _, r in self.rows]
+            window = "run"
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "error": self.err}
+        sm = [num(r[1]) for r in win if len(r) > 2 and num(r[1]) is not None]
+        mx = [num(r[2]) for r in win if len(r) > 2 and num(r[2]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
+        reasons = sorted({n for r in win if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(win), "window": window}
 
 
 def measured_peaks():
@@ -184,6 +205,7 @@ def run_ours(args, rank: int, world: int):
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local).start()
     T = args.tokens
     lib = _native.load()
 
@@ -212,9 +234,18 @@ def run_ours(args, rank: int, world: int):
         if world > 1:
             dist.barrier()
 
-    # ---- warmup
+    # ---- warmup: W steps, then keep stepping (untimed) until ~0.5 s of load so
+    # clocks reach steady state before the timed region
     for i in range(max(args.warmup, 3)):
         step(i)
+    torch.cuda.synchronize()
+    t_w = time.perf_counter()
+    i = 0
+    while time.perf_counter() - t_w < 0.5:
+        step(i)
+        i += 1
+        if i % 50 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
 
     # ---- timed region (device events on the launching stream) with live stage events
@@ -234,15 +265,17 @@ def run_ours(args, rank: int, world: int):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        start.record(stream)
-        for i in range(K):
-            if world == 1:
-                lib.lp_profile_events(ptr_arrays[i], 5)
-            step(i)
-        end.record(stream)
-        torch.cuda.synchronize()
+    t_region0 = time.monotonic()
+    start.record(stream)
+    for i in range(K):
+        if world == 1:
+            lib.lp_profile_events(ptr_arrays[i], 5)
+        step(i)
+    end.record(stream)
+    torch.cuda.synchronize()
+    t_region1 = time.monotonic()
     lib.lp_profile_events(None, 0)
+    clocks.stop()
     barrier()
     ms = start.elapsed_time(end) / K
     if world > 1:
@@ -302,7 +335,7 @@ def run_ours(args, rank: int, world: int):
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                 "d2h_bytes_per_step": T * s.hidden * 2},
         "gpu_launches": 7 * K,
-        "clocks": clocks.summary(),
+        "clocks": clocks.summary(t_region0, t_region1),
     }
     if stage_us is not None:
         nnz = statistics.mean(hits)

@@ -38,6 +38,7 @@ constexpr uint32_t kATileBytes = kTileM * kTileK * 2;  // 16 KiB
 
 struct ExpertsParams {
   int H, I, E;
+  const int32_t* tok_of;       // [S] source row of each slot (nullptr: slot s reads row s)
   const int32_t* offsets;      // [E+1] expert slot offsets
   const int32_t* tile_prefix;  // [E+1] prefix sum of token tiles per expert
   const int32_t* tile_rows;    // [E]   token rows per tile of expert e
@@ -56,7 +57,7 @@ struct ExpertsCfg {
   static constexpr int kTmemCols = kAccStages * kAccCols < 32 ? 32 : kAccStages * kAccCols;
   // barriers + ring + scalars + expert tables
   static constexpr int kAuxBytes = 8 * (2 * kStages + 2 * kAccStages + 2 * kRing) + 16 * kRing + 16 +
-                                   4 * (3 * kMaxExperts + 2);
+                                   4 * (3 * kMaxExperts + 2) + 4 * MAX_N;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
 };
 
@@ -67,7 +68,7 @@ __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(
 template <int MAX_N>
 __global__ void __launch_bounds__(kExpertsThreads, 1)
     k_experts(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
-              const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_act,
+              const __grid_constant__ CUtensorMap tm_xsrc, const __grid_constant__ CUtensorMap tm_act,
               const ExpertsParams p) {
   using C = ExpertsCfg<MAX_N>;
   constexpr int S_ = C::kStages;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   int32_t* s_off = reinterpret_cast<int32_t*>(tmem_slot + 4);
   int32_t* s_tp = s_off + (kMaxExperts + 1);
   int32_t* s_ts = s_tp + (kMaxExperts + 1);
+  int32_t* s_tok = s_ts + kMaxExperts;  // [MAX_N] source rows of the current UP item
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_w13); prefetch_tmap(&tm_w2); prefetch_tmap(&tm_xp); prefetch_tmap(&tm_act);
+    prefetch_tmap(&tm_w13); prefetch_tmap(&tm_w2); prefetch_tmap(&tm_xsrc); prefetch_tmap(&tm_act);
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
   for (int i = threadIdx.x; i <= E; i += blockDim.x) { s_off[i] = p.offsets[i]; s_tp[i] = p.tile_prefix[i]; }
@@ -115,73 +117,86 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   const int n_items = (mt_up + mt_dn) * total_tiles;
 
   if (warp == 0) {
-    // ===================== scheduler + TMA producer =====================
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
-      const uint64_t pol_a = policy_evict_last();   // activations: re-read by every m-tile
-      int stage = 0; uint32_t phase = 0;
-      int r = 0; uint32_t rph = 0;
-      while (true) {
-        const int it = static_cast<int>(atomicAdd(&p.sched[0], 1u));
-        int4 info;
-        int need = 0;
-        if (it >= n_items) {
-          info = make_int4(kItemEnd, 0, 0, 0);
-        } else {
-          const bool up = it < n_up;
-          const int mtc = up ? mt_up : mt_dn;
-          const int local = up ? it : it - n_up;
-          int lo = 0, hi = E;  // largest e with mtc*tp[e] <= local
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (mtc * s_tp[mid] <= local) lo = mid; else hi = mid;
-          }
-          const int e = lo;
-          const int nt_e = s_tp[e + 1] - s_tp[e];
-          const int rr = local - mtc * s_tp[e];
-          const int mt = rr / nt_e, nt = rr - mt * nt_e;
-          const int n_e = s_off[e + 1] - s_off[e];
-          const int ts = s_ts[e];
-          const int row0 = s_off[e] + nt * ts;
-          const int nvalid = min(ts, n_e - nt * ts);
-          info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * kTileM, row0, nvalid);
-          need = mt_up * nt_e;
+    // ===================== scheduler + TMA producer (warp-wide) =====================
+    const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+    const uint64_t pol_a = policy_evict_last();   // activations: re-read by every m-tile
+    int stage = 0; uint32_t phase = 0;
+    int r = 0; uint32_t rph = 0;
+    while (true) {
+      int it = 0;
+      if (lane == 0) it = static_cast<int>(atomicAdd(&p.sched[0], 1u));
+      it = __shfl_sync(0xffffffffu, it, 0);
+      int4 info;
+      int need = 0;
+      if (it >= n_items) {
+        info = make_int4(kItemEnd, 0, 0, 0);
+      } else {
+        const bool up = it < n_up;
+        const int mtc = up ? mt_up : mt_dn;
+        const int local = up ? it : it - n_up;
+        int lo = 0, hi = E;  // largest e with mtc*tp[e] <= local
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (mtc * s_tp[mid] <= local) lo = mid; else hi = mid;
         }
+        const int e = lo;
+        const int nt_e = s_tp[e + 1] - s_tp[e];
+        const int rr = local - mtc * s_tp[e];
+        const int mt = rr / nt_e, nt = rr - mt * nt_e;
+        const int n_e = s_off[e + 1] - s_off[e];
+        const int ts = s_ts[e];
+        const int row0 = s_off[e] + nt * ts;
+        const int nvalid = min(ts, n_e - nt * ts);
+        info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * kTileM, row0, nvalid);
+        need = mt_up * nt_e;
+      }
+      if (lane == 0) {
         mbar_wait(&sempty[r], rph ^ 1);
         ring[r] = info;
         mbar_arrive(&sfull[r]);
-        if (++r == kRing) { r = 0; rph ^= 1; }
-        const int kind = info.x & 0xff;
-        if (kind == kItemEnd) break;
-        const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
+      }
+      if (++r == kRing) { r = 0; rph ^= 1; }
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
+      const int nmma = (nvalid + 15) & ~15;
+      const bool up = kind == kItemUp;
+      if (up) {  // source rows of this item's token tile (pad rows repeat the last valid one)
+        for (int q = lane; q < nmma; q += 32) {
+          const int slot = row0 + min(q, nvalid - 1);
+          s_tok[q] = p.tok_of ? __ldcg(p.tok_of + slot) : slot;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
         const int nbox = (nvalid + kBoxRows - 1) / kBoxRows;
-        if (kind == kItemDown) {
+        if (!up) {
           while (ld_acquire_u32(&p.sched[1 + e]) < static_cast<uint32_t>(need)) __nanosleep(64);
           fence_proxy_async_global();
         }
-        const bool up = kind == kItemUp;
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
-        const uint32_t bytes = (up ? 2 : 1) * kATileBytes + nbox * kBoxRows * 128;
+        const uint32_t bytes = up ? 2 * kATileBytes + nmma * 128 : kATileBytes + nbox * kBoxRows * 128;
         const int arow = up ? e * 2 * p.I + m0 : e * p.H + m0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + 2 * kATileBytes;
           mbar_arrive_expect_tx(&full[stage], bytes);
           if (up) {
             tma_load_2d(sa, &tm_w13, &full[stage], kb * kTileK, arow, pol_w);
             tma_load_2d(sa + kATileBytes, &tm_w13, &full[stage], kb * kTileK, arow + p.I, pol_w);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(sa + 2 * kATileBytes + b * kBoxRows * 128, &tm_xp, &full[stage], kb * kTileK,
-                          row0 + b * kBoxRows, pol_a);
+            for (int g = 0; g < nmma; g += 4)
+              tma_gather4(sb + g * 128, &tm_xsrc, &full[stage], kb * kTileK, s_tok[g], s_tok[g + 1], s_tok[g + 2],
+                          s_tok[g + 3], pol_a);
           } else {
             tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, arow, pol_w);
             for (int b = 0; b < nbox; ++b)
-              tma_load_2d(sa + 2 * kATileBytes + b * kBoxRows * 128, &tm_act, &full[stage], kb * kTileK,
-                          row0 + b * kBoxRows, pol_a);
+              tma_load_2d(sb + b * kBoxRows * 128, &tm_act, &full[stage], kb * kTileK, row0 + b * kBoxRows, pol_a);
           }
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (single thread) =====================

@@ -101,7 +101,7 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
     o = align_up(o + bytes, kAlign);
     return at;
   };
-  L.partial = take(static_cast<size_t>(L.ksplit) * ((E + 127) / 128) * T * E * 4);
+  L.partial = take(static_cast<size_t>(L.ksplit) * ((E + 127) / 128) * T * ((E + 31) / 32 * 32) * 4);
   L.chunk_hist = take(static_cast<size_t>(L.nchunks) * E * 4);
   L.rank_local = take(S * 4);
   L.ids = take(S * 4);
@@ -198,48 +198,44 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
 }
 
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
-int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
-                        int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
-                        const int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows,
-                        uint32_t* sched, cudaStream_t st) {
+int launch_scan(const int32_t* ids, int T, int E, int topk, int32_t* counts, int32_t* offsets, int32_t* slot_of,
+                int32_t* tok_of, int32_t* chunk_hist, const int32_t* rank_local, int max_n, int32_t* tile_prefix,
+                int32_t* tile_rows, uint32_t* sched, cudaStream_t st) {
   const int S = T * topk;
   const int nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
-  lp::k_scan<<<1, 1024, 0, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows, sched);
+  lp::k_scan<<<1, 1024, 0, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows, sched, ids,
+                                 rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of);
   LP_CHECK_LAUNCH("k_scan");
-  lp::k_scatter<<<(S + 7) / 8, 256, 0, st>>>(ids, chunk_hist, rank_local, offsets,
-                                             static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
-                                             lp::kRouterN * topk, slot_of, tok_of,
-                                             static_cast<__nv_bfloat16*>(x_perm));
-  LP_CHECK_LAUNCH("k_scatter");
   return LP_OK;
 }
 
 template <int MAX_N>
-int launch_experts_t(const void* x_perm, const void* act_in, int S, const void* w13, const void* w2, int H, int I,
-                     int E, const lp::ExpertsParams& p, cudaStream_t st) {
+int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, const void* w13, const void* w2,
+                     int H, int I, int E, const lp::ExpertsParams& p, cudaStream_t st) {
   int rc;
   if ((rc = get_encode())) return rc;
-  CUtensorMap tm_w13, tm_w2, tm_xp, tm_act;
+  CUtensorMap tm_w13, tm_w2, tm_xsrc, tm_act;
   if ((rc = make_tmap(&tm_w13, w13, static_cast<uint64_t>(E) * 2 * I, H, lp::kTileM))) return rc;
   if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
-  if ((rc = make_tmap(&tm_xp, x_perm, S, H, lp::kBoxRows))) return rc;
+  if ((rc = make_tmap(&tm_xsrc, src, src_rows, H, 1))) return rc;  // gather4 rows
   if ((rc = make_tmap(&tm_act, act_in, S, I, lp::kBoxRows))) return rc;
   constexpr int smem = lp::ExpertsCfg<MAX_N>::kSmemBytes;
   if ((rc = set_smem(lp::k_experts<MAX_N>, smem))) return rc;
-  lp::k_experts<MAX_N><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xp, tm_act, p);
+  lp::k_experts<MAX_N><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xsrc, tm_act, p);
   LP_CHECK_LAUNCH("k_experts");
   return LP_OK;
 }
 
-int launch_experts(const void* x_perm, int S, const void* w13, const void* w2, int H, int I, int E, int max_n,
-                   const int32_t* offsets, const int32_t* tile_prefix, const int32_t* tile_rows, uint32_t* sched,
-                   void* act, void* y_perm, cudaStream_t st) {
-  lp::ExpertsParams p{H, I, E, offsets, tile_prefix, tile_rows, static_cast<__nv_bfloat16*>(act),
+// src: [src_rows, H] token rows; slot s reads row tok_of[s] (tok_of == nullptr: row s).
+int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, const void* w13, const void* w2,
+                   int H, int I, int E, int max_n, const int32_t* offsets, const int32_t* tile_prefix,
+                   const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st) {
+  lp::ExpertsParams p{H, I, E, tok_of, offsets, tile_prefix, tile_rows, static_cast<__nv_bfloat16*>(act),
                       static_cast<__nv_bfloat16*>(y_perm), sched};
   switch (max_n) {
-    case 64: return launch_experts_t<64>(x_perm, act, S, w13, w2, H, I, E, p, st);
-    case 128: return launch_experts_t<128>(x_perm, act, S, w13, w2, H, I, E, p, st);
-    default: return launch_experts_t<256>(x_perm, act, S, w13, w2, H, I, E, p, st);
+    case 64: return launch_experts_t<64>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    case 128: return launch_experts_t<128>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    default: return launch_experts_t<256>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
   }
 }
 
@@ -327,10 +323,15 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   lp::k_chunk_hist<<<(L.nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
                      lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, T * topk, E, chunk, chunk_hist, rank_local);
   LP_CHECK_LAUNCH("k_chunk_hist");
-  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm, chunk_hist,
-                                rank_local, max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
-                                at<uint32_t>(ws, L.sched), st)))
+  if ((rc = launch_scan(ids, T, E, topk, counts, offsets, slot_of, tok_of, chunk_hist, rank_local, max_n,
+                        at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
     return rc;
+  if (x_perm) {
+    const int S = T * topk;
+    lp::k_gather_rows<<<(S + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), tok_of, S, H,
+                                                   static_cast<__nv_bfloat16*>(x_perm));
+    LP_CHECK_LAUNCH("k_gather_rows");
+  }
   return ok();
 }
 
@@ -355,7 +356,8 @@ int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void
   const int sb = (E + 31) / 32 * 32;
   k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
   LP_CHECK_LAUNCH("k_plan");
-  if ((rc = launch_experts(x_perm, S, w13, w2, H, I, E, max_n, offsets, tile_prefix, tile_rows, sched, act, y_perm,
+  if ((rc = launch_experts(x_perm, S, nullptr, S, w13, w2, H, I, E, max_n, offsets, tile_prefix, tile_rows, sched,
+                           act, y_perm,
                            st)))
     return rc;
   return ok();
@@ -395,13 +397,13 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   prof_mark(0, st);
   if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
   prof_mark(1, st);
-  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, at<int32_t>(ws, L.tok_of),
-                                at<void>(ws, L.x_perm), at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local),
-                                max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
-                                at<uint32_t>(ws, L.sched), st)))
+  int32_t* tok_of = at<int32_t>(ws, L.tok_of);
+  if ((rc = launch_scan(ids, T, E, topk, counts, offsets, slot_of, tok_of, at<int32_t>(ws, L.chunk_hist),
+                        at<int32_t>(ws, L.rank_local), max_n, at<int32_t>(ws, L.tile_prefix),
+                        at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
     return rc;
   prof_mark(2, st);
-  if ((rc = launch_experts(at<void>(ws, L.x_perm), S, w13, w2, H, I, E, max_n, offsets, at<int32_t>(ws, L.tile_prefix),
+  if ((rc = launch_experts(x, T, tok_of, S, w13, w2, H, I, E, max_n, offsets, at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
                            at<void>(ws, L.y_perm), st)))
     return rc;

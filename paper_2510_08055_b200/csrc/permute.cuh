@@ -7,11 +7,12 @@
 // tokens (`torch.where(expert_mask[e])`, modeling_qwen3_moe.py:243) and the
 // order the oracle's stable argsort produces, so slot_of is bit-exact.
 //
-// Histogram: one warp per chunk of kChunk entries, __match_any_sync for the
-// in-warp rank, a per-warp smem counter table for the running rank. The scan
-// kernel turns per-chunk counts into per-chunk bases (fixed order), computes
-// offsets and the token-tile schedule the expert kernel consumes, and resets
-// the expert kernel's scheduler words (so the whole layer stays graph-capturable).
+// Chunks are the router's 32-token tiles: the router kernel (route.cuh) emits
+// each tile's expert histogram and in-tile stable ranks. One single-block scan
+// kernel turns the per-tile counts into per-tile bases (fixed order), the
+// expert offsets, every entry's slot (slot_of) and its inverse (tok_of), the
+// token-tile schedule the expert kernel consumes, and resets the expert
+// kernel's scheduler words (the whole layer stays graph-capturable).
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -60,10 +61,12 @@ __global__ void __launch_bounds__(32 * kHistWarps)
 __global__ void __launch_bounds__(1024)
     k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n, int32_t* __restrict__ counts,
            int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
-           uint32_t* __restrict__ sched) {
+           uint32_t* __restrict__ sched, const int32_t* __restrict__ ids, const int32_t* __restrict__ rank_local,
+           int S, int topk, int chunk, int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of) {
   __shared__ int32_t s_part[1024];
   __shared__ int32_t s_cnt[256];
   __shared__ int32_t s_til[256];
+  __shared__ int32_t s_off[256];
   const int e_pad = (E + 31) & ~31;
   const int G = blockDim.x / e_pad;
   const int g = threadIdx.x / e_pad;
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(1024)
   }
   if (me < E) {
     offsets[me] = s_cnt[me] - cnt;
+    s_off[me] = s_cnt[me] - cnt;
     tile_prefix[me] = s_til[me] - ntiles;
     const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
     tile_rows[me] = min(max_n, (rows + 15) & ~15);
@@ -128,30 +132,28 @@ __global__ void __launch_bounds__(1024)
     }
   }
   for (int i = threadIdx.x; i <= E; i += blockDim.x) sched[i] = 0u;
+  __syncthreads();
+  // expert-contiguous slot of every routing entry and its inverse (slot -> token)
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    const int ex = __ldcg(ids + i);
+    const int slot = s_off[ex] + __ldcg(chunk_hist + static_cast<size_t>(i / chunk) * E + ex) + __ldcg(rank_local + i);
+    slot_of[i] = slot;
+    tok_of[slot] = i / topk;
+  }
 }
 
-// One warp per routing entry: final slot, inverse map, and the row gather.
+// x_perm[slot] = x[tok_of[slot]] (standalone lp_moe_permute only; the fused
+// forward never materialises x_perm — the expert kernel gathers rows by TMA).
 __global__ void __launch_bounds__(256)
-    k_scatter(const int32_t* __restrict__ ids, const int32_t* __restrict__ chunk_base,
-              const int32_t* __restrict__ rank_local, const int32_t* __restrict__ offsets,
-              const __nv_bfloat16* __restrict__ x, int S, int E, int topk, int H, int chunk,
-              int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of, __nv_bfloat16* __restrict__ x_perm) {
-  const int i = blockIdx.x * 8 + threadIdx.x / 32;
+    k_gather_rows(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ tok_of, int S, int H,
+                  __nv_bfloat16* __restrict__ x_perm) {
+  const int slot = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (i >= S) return;
-  const int e = ids[i];
-  const int t = i / topk;
-  const int slot = offsets[e] + chunk_base[static_cast<size_t>(i / chunk) * E + e] + rank_local[i];
-  if (lane == 0) {
-    slot_of[i] = slot;
-    tok_of[slot] = t;
-  }
-  if (x_perm != nullptr) {
-    const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
-    uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
-    const int nv = H / 8;
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
-  }
+  if (slot >= S) return;
+  const int t = tok_of[slot];
+  const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+  uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
+  for (int v = lane; v < H / 8; v += 32) dst[v] = src[v];
 }
 
 // y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]]   (fp32 accumulate in fixed j order, bf16 out)

@@ -35,7 +35,7 @@ struct RouterParams {
   int ksplit;        // number of H slices
   int kb_split;      // 64-wide K blocks per slice
   int mtiles;        // ceil(E / 128)
-  float* partial;    // [ksplit * mtiles, T, E] (unused when ksplit*mtiles == 1)
+  float* partial;    // [ksplit * mtiles, T, E_pad] (unused when ksplit*mtiles == 1)
   uint32_t* ticket;  // [ntiles], zero between calls (self-resetting)
   int32_t* ids;      // [T, topk]
   float* w;          // [T, topk]
@@ -125,12 +125,13 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     }
     bool last = true;
     if (arrivals > 1) {
+      // partial rows are padded to e_pad so the reduction can use float4 loads
       const int slice = split * p.mtiles + mt;
-      float* dst = p.partial + (static_cast<size_t>(slice) * p.T) * p.E;
+      float* dst = p.partial + (static_cast<size_t>(slice) * p.T) * e_pad;
 #pragma unroll
       for (int i = 0; i < kRouterN; ++i) {
         const int t = t0 + i;
-        if (t < p.T && e < p.E) dst[static_cast<size_t>(t) * p.E + e] = __uint_as_float(v[i]);
+        if (t < p.T && e < e_pad) dst[static_cast<size_t>(t) * e_pad + e] = __uint_as_float(v[i]);
       }
       __threadfence();
       named_bar_sync(1, 128);
@@ -143,19 +144,44 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       if (last) {
         __threadfence();
         if (et == 0) p.ticket[nt] = 0u;  // ready for the next call
-        // fixed-order reduction of all slices: s_logit[t][e]
-        for (int ee = et; ee < e_pad; ee += 128) {
-          for (int i = 0; i < kRouterN; ++i) {
-            const int t = t0 + i;
-            float acc = 0.f;
-            if (t < p.T && ee < p.E) {
-              const int emt = ee >> 7;
-              for (int sp = 0; sp < p.ksplit; ++sp)
-                acc += __ldcg(p.partial + (static_cast<size_t>(sp * p.mtiles + emt) * p.T + t) * p.E + ee);
+        // Fixed-order reduction of the slices into s_logit[t][e]. Warp q owns
+        // tokens q*8..q*8+7, lane owns 4 consecutive experts (float4); all
+        // slices of two tokens are loaded before any is summed.
+        const int nslices = arrivals;
+        for (int eb = 4 * lane; eb < e_pad; eb += 128) {
+          const int emt = eb >> 7;
+#pragma unroll 1
+          for (int i = q * 8; i < q * 8 + 8; i += 2) {
+            float4 part[2][kRouterMaxSplit];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int t = min(t0 + i + u, p.T - 1);
+#pragma unroll
+              for (int sp = 0; sp < kRouterMaxSplit; ++sp) {
+                if (sp < p.ksplit) {
+                  const int sl = sp * p.mtiles + emt;
+                  part[u][sp] = __ldcg(reinterpret_cast<const float4*>(
+                      p.partial + (static_cast<size_t>(sl) * p.T + t) * e_pad + eb));
+                } else {
+                  part[u][sp] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
             }
-            s_logit[i * e_pad + ee] = acc;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int sp = 0; sp < kRouterMaxSplit; ++sp) {
+                if (sp < p.ksplit) {
+                  acc.x += part[u][sp].x; acc.y += part[u][sp].y;
+                  acc.z += part[u][sp].z; acc.w += part[u][sp].w;
+                }
+              }
+              *reinterpret_cast<float4*>(s_logit + (i + u) * e_pad + eb) = acc;
+            }
           }
         }
+        (void)nslices;
       }
     } else {
 #pragma unroll
