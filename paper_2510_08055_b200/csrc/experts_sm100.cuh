@@ -65,7 +65,10 @@ enum : int { kItemUp = 0, kItemDown = 1, kItemEnd = 2 };
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
-template <int MAX_N>
+// GATHER: UP items read token rows of an unpermuted [rows, H] source through
+// TMA tile::gather4 (tok_of indices); otherwise rows are expert-contiguous
+// (x_perm) and arrive in 32-row TMA boxes.
+template <int MAX_N, bool GATHER>
 __global__ void __launch_bounds__(kExpertsThreads, 1)
     k_experts(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
               const __grid_constant__ CUtensorMap tm_xsrc, const __grid_constant__ CUtensorMap tm_act,
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
       const int nmma = (nvalid + 15) & ~15;
       const bool up = kind == kItemUp;
-      if (up) {  // source rows of this item's token tile (pad rows repeat the last valid one)
+      if (GATHER && up) {  // source rows of this item's token tile (pad rows repeat the last valid one)
         for (int q = lane; q < nmma; q += 32) {
           const int slot = row0 + min(q, nvalid - 1);
           s_tok[q] = p.tok_of ? __ldcg(p.tok_of + slot) : slot;
@@ -175,7 +178,8 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           fence_proxy_async_global();
         }
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
-        const uint32_t bytes = up ? 2 * kATileBytes + nmma * 128 : kATileBytes + nbox * kBoxRows * 128;
+        const uint32_t bytes = up ? 2 * kATileBytes + (GATHER ? nmma * 128 : nbox * kBoxRows * 128)
+                                  : kATileBytes + nbox * kBoxRows * 128;
         const int arow = up ? e * 2 * p.I + m0 : e * p.H + m0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -185,9 +189,15 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           if (up) {
             tma_load_2d(sa, &tm_w13, &full[stage], kb * kTileK, arow, pol_w);
             tma_load_2d(sa + kATileBytes, &tm_w13, &full[stage], kb * kTileK, arow + p.I, pol_w);
-            for (int g = 0; g < nmma; g += 4)
-              tma_gather4(sb + g * 128, &tm_xsrc, &full[stage], kb * kTileK, s_tok[g], s_tok[g + 1], s_tok[g + 2],
-                          s_tok[g + 3], pol_a);
+            if (GATHER) {
+              for (int g = 0; g < nmma; g += 4)
+                tma_gather4(sb + g * 128, &tm_xsrc, &full[stage], kb * kTileK, s_tok[g], s_tok[g + 1],
+                            s_tok[g + 2], s_tok[g + 3], pol_a);
+            } else {
+              for (int b = 0; b < nbox; ++b)
+                tma_load_2d(sb + b * kBoxRows * 128, &tm_xsrc, &full[stage], kb * kTileK, row0 + b * kBoxRows,
+                            pol_a);
+            }
           } else {
             tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, arow, pol_w);
             for (int b = 0; b < nbox; ++b)

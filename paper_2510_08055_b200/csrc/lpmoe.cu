@@ -58,17 +58,6 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ------------------------------------------------------------------ shapes
-int router_ksplit(int T, int H, int E) {
-  const int kb_total = H / 64;
-  const int base = ((T + lp::kRouterN - 1) / lp::kRouterN) * ((E + 127) / 128);
-  int ks = kTargetCtas / (base > 0 ? base : 1);
-  if (ks < 1) ks = 1;
-  if (ks > lp::kRouterMaxSplit) ks = lp::kRouterMaxSplit;
-  if (ks > kb_total) ks = kb_total;
-  while (kb_total % ks) --ks;  // slices of equal K length
-  return ks;
-}
-
 int pick_max_n(int S, int E) {
   const int avg = (S + E - 1) / E;
   if (avg <= 40) return 64;
@@ -85,15 +74,14 @@ constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB of ticket
 constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E+1 <= 257)
 
 struct Layout {
-  size_t partial, chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
+  size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
   size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
-  int ksplit, nchunks;
+  int nchunks;
 };
 
 Layout make_layout(int T, int H, int I, int E, int topk) {
   Layout L{};
   const size_t S = static_cast<size_t>(T) * topk;
-  L.ksplit = router_ksplit(T, H, E);
   L.nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
   size_t o = kHeaderBytes;
   auto take = [&](size_t bytes) {
@@ -101,7 +89,6 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
     o = align_up(o + bytes, kAlign);
     return at;
   };
-  L.partial = take(static_cast<size_t>(L.ksplit) * ((E + 127) / 128) * T * ((E + 31) / 32 * 32) * 4);
   L.chunk_hist = take(static_cast<size_t>(L.nchunks) * E * 4);
   L.rank_local = take(S * 4);
   L.ids = take(S * 4);
@@ -162,6 +149,11 @@ int make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uin
   return LP_OK;
 }
 
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
 // ------------------------------------------------------------------ device info
 int sm_count() {
   int dev = 0, n = 0;
@@ -185,14 +177,12 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   CUtensorMap tm_wr, tm_x;
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
   if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
-  char* base = static_cast<char*>(ws);
-  lp::RouterParams rp{T, H, E, topk, renorm, L.ksplit, (H / 64) / L.ksplit, (E + 127) / 128,
-                      reinterpret_cast<float*>(base + L.partial), reinterpret_cast<uint32_t*>(base + kTicketOff), ids,
-                      w, reinterpret_cast<int32_t*>(base + L.chunk_hist),
-                      reinterpret_cast<int32_t*>(base + L.rank_local)};
-  if ((rc = set_smem(lp::k_router, lp::kRouterSmem))) return rc;
-  const int grid = L.nchunks * rp.mtiles * L.ksplit;
-  lp::k_router<<<grid, lp::kRouterThreads, lp::kRouterSmem, st>>>(tm_wr, tm_x, rp);
+  const int mtiles = (E + 127) / 128;
+  lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
+                      at<int32_t>(ws, L.rank_local)};
+  const int smem = lp::router_smem_bytes(mtiles);
+  if ((rc = set_smem(lp::k_router, smem))) return rc;
+  lp::k_router<<<L.nchunks, lp::kRouterThreads, smem, st>>>(tm_wr, tm_x, rp);
   LP_CHECK_LAUNCH("k_router");
   return LP_OK;
 }
@@ -203,13 +193,19 @@ int launch_scan(const int32_t* ids, int T, int E, int topk, int32_t* counts, int
                 int32_t* tile_rows, uint32_t* sched, cudaStream_t st) {
   const int S = T * topk;
   const int nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
-  lp::k_scan<<<1, 1024, 0, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows, sched, ids,
-                                 rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of);
+  const int n_hist = nchunks * E;
+  const int smem = n_hist <= lp::kScanSmemInts ? n_hist * 4 : 0;
+  if (smem > 48 * 1024) {
+    int rc;
+    if ((rc = set_smem(lp::k_scan, lp::kScanSmemInts * 4))) return rc;
+  }
+  lp::k_scan<<<1, lp::kScanThreads, smem, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows,
+                                                sched, ids, rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of);
   LP_CHECK_LAUNCH("k_scan");
   return LP_OK;
 }
 
-template <int MAX_N>
+template <int MAX_N, bool GATHER>
 int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, const void* w13, const void* w2,
                      int H, int I, int E, const lp::ExpertsParams& p, cudaStream_t st) {
   int rc;
@@ -217,11 +213,11 @@ int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, c
   CUtensorMap tm_w13, tm_w2, tm_xsrc, tm_act;
   if ((rc = make_tmap(&tm_w13, w13, static_cast<uint64_t>(E) * 2 * I, H, lp::kTileM))) return rc;
   if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
-  if ((rc = make_tmap(&tm_xsrc, src, src_rows, H, 1))) return rc;  // gather4 rows
+  if ((rc = make_tmap(&tm_xsrc, src, src_rows, H, GATHER ? 1 : lp::kBoxRows))) return rc;
   if ((rc = make_tmap(&tm_act, act_in, S, I, lp::kBoxRows))) return rc;
   constexpr int smem = lp::ExpertsCfg<MAX_N>::kSmemBytes;
-  if ((rc = set_smem(lp::k_experts<MAX_N>, smem))) return rc;
-  lp::k_experts<MAX_N><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xsrc, tm_act, p);
+  if ((rc = set_smem(lp::k_experts<MAX_N, GATHER>, smem))) return rc;
+  lp::k_experts<MAX_N, GATHER><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xsrc, tm_act, p);
   LP_CHECK_LAUNCH("k_experts");
   return LP_OK;
 }
@@ -232,10 +228,17 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
                    const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st) {
   lp::ExpertsParams p{H, I, E, tok_of, offsets, tile_prefix, tile_rows, static_cast<__nv_bfloat16*>(act),
                       static_cast<__nv_bfloat16*>(y_perm), sched};
+  if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
+    switch (max_n) {
+      case 64: return launch_experts_t<64, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+      case 128: return launch_experts_t<128, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+      default: return launch_experts_t<256, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    }
+  }
   switch (max_n) {
-    case 64: return launch_experts_t<64>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
-    case 128: return launch_experts_t<128>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
-    default: return launch_experts_t<256>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    case 64: return launch_experts_t<64, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    case 128: return launch_experts_t<128, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
+    default: return launch_experts_t<256, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
   }
 }
 
@@ -263,10 +266,6 @@ __global__ void k_plan(const int32_t* __restrict__ offsets, int E, int max_n, in
   for (int i = e; i <= E; i += blockDim.x) sched[i] = 0u;
 }
 
-template <typename T>
-T* at(void* ws, size_t off) {
-  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
-}
 
 }  // namespace
 
@@ -403,7 +402,11 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
                         at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
     return rc;
   prof_mark(2, st);
-  if ((rc = launch_experts(x, T, tok_of, S, w13, w2, H, I, E, max_n, offsets, at<int32_t>(ws, L.tile_prefix),
+  lp::k_gather_rows<<<(S + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), tok_of, S, H,
+                                                 at<__nv_bfloat16>(ws, L.x_perm));
+  LP_CHECK_LAUNCH("k_gather_rows");
+  if ((rc = launch_experts(at<void>(ws, L.x_perm), S, nullptr, S, w13, w2, H, I, E, max_n, offsets,
+                           at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
                            at<void>(ws, L.y_perm), st)))
     return rc;

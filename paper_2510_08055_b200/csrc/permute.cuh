@@ -53,92 +53,121 @@ __global__ void __launch_bounds__(32 * kHistWarps)
   }
 }
 
-// Single block of 1024 threads: G = 1024/E_pad groups of E_pad threads; group g
-// owns a contiguous range of chunks. Pass 1 sums the range, the G partial sums
-// are scanned, pass 2 rewrites chunk_hist in place as per-chunk exclusive bases
-// (fixed order). Then offsets, the expert kernel's token-tile schedule, and the
-// reset of its scheduler words.
-__global__ void __launch_bounds__(1024)
+// Single block of 1024 threads. The per-tile histograms are staged in shared
+// memory when they fit (nchunks*E <= kScanSmemInts, i.e. T <= ~3k tokens for
+// E=128), otherwise scanned in place in global memory. G = 1024/E_pad groups of
+// E_pad threads; group g owns a contiguous range of tiles: pass 1 sums the
+// range, the G partial sums are scanned, pass 2 rewrites the histograms as
+// per-tile exclusive bases (fixed order). Then offsets, every entry's slot
+// (slot_of) and inverse (tok_of), the expert kernel's token-tile schedule, and
+// the reset of its scheduler words.
+constexpr int kScanThreads = 1024;
+constexpr int kScanSmemInts = 24576;  // 96 KiB
+
+__global__ void __launch_bounds__(kScanThreads)
     k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n, int32_t* __restrict__ counts,
            int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
            uint32_t* __restrict__ sched, const int32_t* __restrict__ ids, const int32_t* __restrict__ rank_local,
            int S, int topk, int chunk, int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of) {
-  __shared__ int32_t s_part[1024];
+  extern __shared__ int32_t s_hist[];
+  __shared__ int32_t s_part[kScanThreads];
   __shared__ int32_t s_cnt[256];
   __shared__ int32_t s_til[256];
   __shared__ int32_t s_off[256];
+  const int tid = threadIdx.x;
   const int e_pad = (E + 31) & ~31;
-  const int G = blockDim.x / e_pad;
-  const int g = threadIdx.x / e_pad;
-  const int e = threadIdx.x % e_pad;
+  const int G = kScanThreads / e_pad;
+  const int g = tid / e_pad;
+  const int e = tid % e_pad;
+  const int n_hist = nchunks * E;
+  const bool staged = n_hist <= kScanSmemInts;
+  int32_t* hist = staged ? s_hist : chunk_hist;
+  if (staged) {
+    for (int i = tid; i < n_hist; i += 4 * kScanThreads) {
+      int v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (i + u * kScanThreads < n_hist) ? __ldcg(chunk_hist + i + u * kScanThreads) : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u * kScanThreads < n_hist) s_hist[i + u * kScanThreads] = v[u];
+    }
+    __syncthreads();
+  }
   const int per = (nchunks + G - 1) / G;
   const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
   int sum = 0;
   if (g < G && e < E) {
-    int c = c0;
-    for (; c + 4 <= c1; c += 4) {
-      sum += __ldcg(chunk_hist + static_cast<size_t>(c) * E + e) + __ldcg(chunk_hist + static_cast<size_t>(c + 1) * E + e) +
-             __ldcg(chunk_hist + static_cast<size_t>(c + 2) * E + e) + __ldcg(chunk_hist + static_cast<size_t>(c + 3) * E + e);
-    }
-    for (; c < c1; ++c) sum += __ldcg(chunk_hist + static_cast<size_t>(c) * E + e);
+    for (int c = c0; c < c1; ++c) sum += staged ? hist[c * E + e] : __ldcg(hist + static_cast<size_t>(c) * E + e);
   }
   if (g < G) s_part[g * e_pad + e] = sum;
   __syncthreads();
-  if (threadIdx.x < e_pad) {
+  if (tid < e_pad) {
     int run = 0;
     for (int gg = 0; gg < G; ++gg) {
-      const int v = s_part[gg * e_pad + threadIdx.x];
-      s_part[gg * e_pad + threadIdx.x] = run;
+      const int v = s_part[gg * e_pad + tid];
+      s_part[gg * e_pad + tid] = run;
       run += v;
     }
-    s_cnt[threadIdx.x] = (threadIdx.x < E) ? run : 0;
+    s_cnt[tid] = (tid < E) ? run : 0;
   }
   __syncthreads();
   if (g < G && e < E) {
     int run = s_part[g * e_pad + e];
     for (int c = c0; c < c1; ++c) {
       const size_t at = static_cast<size_t>(c) * E + e;
-      const int v = __ldcg(chunk_hist + at);
-      chunk_hist[at] = run;
+      const int v = staged ? hist[at] : __ldcg(hist + at);
+      hist[at] = run;
       run += v;
     }
   }
   // offsets / tile schedule over experts (e_pad <= 256 threads)
-  const int me = threadIdx.x;
   int cnt = 0, ntiles = 0;
-  if (me < e_pad) {
-    cnt = s_cnt[me];
+  if (tid < e_pad) {
+    cnt = s_cnt[tid];
     ntiles = (cnt > 0) ? (cnt + max_n - 1) / max_n : 0;
-    s_til[me] = ntiles;
-    if (me < E) counts[me] = cnt;
+    s_til[tid] = ntiles;
+    if (tid < E) counts[tid] = cnt;
   }
   __syncthreads();
   for (int o = 1; o < e_pad; o <<= 1) {
     int a = 0, b = 0;
-    if (me < e_pad && me >= o) { a = s_cnt[me - o]; b = s_til[me - o]; }
+    if (tid < e_pad && tid >= o) { a = s_cnt[tid - o]; b = s_til[tid - o]; }
     __syncthreads();
-    if (me < e_pad) { s_cnt[me] += a; s_til[me] += b; }
+    if (tid < e_pad) { s_cnt[tid] += a; s_til[tid] += b; }
     __syncthreads();
   }
-  if (me < E) {
-    offsets[me] = s_cnt[me] - cnt;
-    s_off[me] = s_cnt[me] - cnt;
-    tile_prefix[me] = s_til[me] - ntiles;
+  if (tid < E) {
+    offsets[tid] = s_cnt[tid] - cnt;
+    s_off[tid] = s_cnt[tid] - cnt;
+    tile_prefix[tid] = s_til[tid] - ntiles;
     const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
-    tile_rows[me] = min(max_n, (rows + 15) & ~15);
-    if (me == E - 1) {
-      offsets[E] = s_cnt[me];
-      tile_prefix[E] = s_til[me];
+    tile_rows[tid] = min(max_n, (rows + 15) & ~15);
+    if (tid == E - 1) {
+      offsets[E] = s_cnt[tid];
+      tile_prefix[E] = s_til[tid];
     }
   }
-  for (int i = threadIdx.x; i <= E; i += blockDim.x) sched[i] = 0u;
+  for (int i = tid; i <= E; i += kScanThreads) sched[i] = 0u;
   __syncthreads();
   // expert-contiguous slot of every routing entry and its inverse (slot -> token)
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    const int ex = __ldcg(ids + i);
-    const int slot = s_off[ex] + __ldcg(chunk_hist + static_cast<size_t>(i / chunk) * E + ex) + __ldcg(rank_local + i);
-    slot_of[i] = slot;
-    tok_of[slot] = i / topk;
+  for (int i0 = tid; i0 < S; i0 += 4 * kScanThreads) {
+    int ex[4], rl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kScanThreads;
+      ex[u] = (i < S) ? __ldcg(ids + i) : -1;
+      rl[u] = (i < S) ? __ldcg(rank_local + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kScanThreads;
+      if (ex[u] >= 0) {
+        const size_t at = static_cast<size_t>(i / chunk) * E + ex[u];
+        const int slot = s_off[ex[u]] + (staged ? hist[at] : __ldcg(hist + at)) + rl[u];
+        slot_of[i] = slot;
+        tok_of[slot] = i / topk;
+      }
+    }
   }
 }
 
