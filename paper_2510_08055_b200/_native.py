@@ -16,7 +16,7 @@ import threading
 from .types import ValidationError
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "liblpmoe.so")
+LIB_PATH = os.environ.get("LPMOE_LIB") or os.path.join(LIB_DIR, "liblpmoe.so")  # override: trace builds
 
 LP_OK = 0
 LP_EINVAL = 1

@@ -40,6 +40,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+TRACE_OUT = os.path.join(PKG, "_lib", "liblpmoe_trace.so")
+
+
+def build_trace(verbose: bool = False) -> str:
+    """Instrumented variant (-DLP_TRACE) for tools/trace_layer.py; never loaded by the package."""
+    os.makedirs(os.path.dirname(TRACE_OUT), exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, "-DLP_TRACE", "-o", TRACE_OUT] + [os.path.join(CSRC, s) for s in SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+    return TRACE_OUT
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
@@ -57,3 +70,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--trace" in sys.argv:
+        print(build_trace(verbose=True))

@@ -45,6 +45,7 @@ struct ExpertsParams {
   __nv_bfloat16* act;          // [S, I]
   __nv_bfloat16* y_perm;       // [S, H]
   uint32_t* sched;             // [0] work counter, [1+e] UP items done for expert e
+  int prefetch_kblocks;        // k-blocks of the first item's W13 rows to warm in L2 before pdl_wait
 };
 
 template <int MAX_N>
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
   const int E = p.E;
+  if (threadIdx.x == 0) { LP_TRACE_MIN(32); LP_TRACE_AT(blockIdx.x == 0, 33); }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -104,8 +106,23 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_w13); prefetch_tmap(&tm_w2); prefetch_tmap(&tm_xsrc); prefetch_tmap(&tm_act);
+    // While the predecessors (router / scan / gather) finish, warm L2 with the
+    // first k-blocks of this CTA's first work item (item == blockIdx.x), guessed
+    // assuming one token tile per expert — exact in the memory-bound regime.
+    const int mt_up0 = p.I / kTileM;
+    const int e_guess = blockIdx.x / mt_up0;
+    if (e_guess < E) {
+      const int row = e_guess * 2 * p.I + (blockIdx.x % mt_up0) * kTileM;
+      const int kb_pf = min(p.prefetch_kblocks, p.H / kTileK);
+      for (int kb = 0; kb < kb_pf; ++kb) {
+        tma_prefetch_2d(&tm_w13, kb * kTileK, row);
+        tma_prefetch_2d(&tm_w13, kb * kTileK, row + p.I);
+      }
+    }
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  pdl_trigger();
+  pdl_wait();
   for (int i = threadIdx.x; i <= E; i += blockDim.x) { s_off[i] = p.offsets[i]; s_tp[i] = p.tile_prefix[i]; }
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_ts[i] = p.tile_rows[i];
   tc_fence_before();
@@ -125,9 +142,11 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     const uint64_t pol_a = policy_evict_last();   // activations: re-read by every m-tile
     int stage = 0; uint32_t phase = 0;
     int r = 0; uint32_t rph = 0;
+    bool first = true;
     while (true) {
-      int it = 0;
-      if (lane == 0) it = static_cast<int>(atomicAdd(&p.sched[0], 1u));
+      int it = 0;  // first item static (matches the L2 prefetch), then dynamic
+      if (lane == 0) it = first ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x + atomicAdd(&p.sched[0], 1u));
+      first = false;
       it = __shfl_sync(0xffffffffu, it, 0);
       int4 info;
       int need = 0;
@@ -311,6 +330,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) { LP_TRACE_MAX(34); LP_TRACE_AT(blockIdx.x == 0, 35); }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <utility>
 
 #include "../../include/lpmoe.h"
 #include "experts_sm100.cuh"
@@ -162,6 +163,24 @@ int sm_count() {
   return n;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while its stream predecessor drains; kernels pdl_wait() before global I/O.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <typename K>
 int set_smem(K kernel, int bytes) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -182,8 +201,7 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
                       at<int32_t>(ws, L.rank_local)};
   const int smem = lp::router_smem_bytes(mtiles);
   if ((rc = set_smem(lp::k_router, smem))) return rc;
-  lp::k_router<<<L.nchunks, lp::kRouterThreads, smem, st>>>(tm_wr, tm_x, rp);
-  LP_CHECK_LAUNCH("k_router");
+  LP_CUDA(launch_pdl(lp::k_router, L.nchunks, lp::kRouterThreads, smem, st, tm_wr, tm_x, rp));
   return LP_OK;
 }
 
@@ -199,9 +217,8 @@ int launch_scan(const int32_t* ids, int T, int E, int topk, int32_t* counts, int
     int rc;
     if ((rc = set_smem(lp::k_scan, lp::kScanSmemInts * 4))) return rc;
   }
-  lp::k_scan<<<1, lp::kScanThreads, smem, st>>>(chunk_hist, nchunks, E, max_n, counts, offsets, tile_prefix, tile_rows,
-                                                sched, ids, rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of);
-  LP_CHECK_LAUNCH("k_scan");
+  LP_CUDA(launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts, offsets,
+                     tile_prefix, tile_rows, sched, ids, rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of));
   return LP_OK;
 }
 
@@ -217,17 +234,20 @@ int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, c
   if ((rc = make_tmap(&tm_act, act_in, S, I, lp::kBoxRows))) return rc;
   constexpr int smem = lp::ExpertsCfg<MAX_N>::kSmemBytes;
   if ((rc = set_smem(lp::k_experts<MAX_N, GATHER>, smem))) return rc;
-  lp::k_experts<MAX_N, GATHER><<<sm_count(), lp::kExpertsThreads, smem, st>>>(tm_w13, tm_w2, tm_xsrc, tm_act, p);
-  LP_CHECK_LAUNCH("k_experts");
+  LP_CUDA(launch_pdl(lp::k_experts<MAX_N, GATHER>, sm_count(), lp::kExpertsThreads, smem, st, tm_w13, tm_w2, tm_xsrc,
+                     tm_act, p));
   return LP_OK;
 }
+
+constexpr int kPrefetchKBlocks = 16;  // 2 x 16 x 16 KiB = 0.5 MiB of W13 per CTA warmed before pdl_wait
 
 // src: [src_rows, H] token rows; slot s reads row tok_of[s] (tok_of == nullptr: row s).
 int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, const void* w13, const void* w2,
                    int H, int I, int E, int max_n, const int32_t* offsets, const int32_t* tile_prefix,
                    const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st) {
-  lp::ExpertsParams p{H, I, E, tok_of, offsets, tile_prefix, tile_rows, static_cast<__nv_bfloat16*>(act),
-                      static_cast<__nv_bfloat16*>(y_perm), sched};
+  lp::ExpertsParams p{H,       I,           E,        tok_of, offsets, tile_prefix, tile_rows,
+                      static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
+                      kPrefetchKBlocks};
   if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
     switch (max_n) {
       case 64: return launch_experts_t<64, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
@@ -368,9 +388,8 @@ int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, i
   if (T == 0) return ok();
   if (!y_perm || !slot_of || !w || !y) return fail(LP_EINVAL, "lp_moe_combine: null pointer argument");
   if (H / 8 > 32 * lp::kCombineThreads) return fail(LP_EUNSUPPORTED, "lp_moe_combine: H too large");
-  lp::k_combine<<<T, lp::kCombineThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(y_perm), slot_of, w, T, topk, H, static_cast<__nv_bfloat16*>(y));
-  LP_CHECK_LAUNCH("k_combine");
+  LP_CUDA(launch_pdl(lp::k_combine, T, lp::kCombineThreads, 0, static_cast<cudaStream_t>(stream),
+                     static_cast<const __nv_bfloat16*>(y_perm), slot_of, w, T, topk, H, static_cast<__nv_bfloat16*>(y)));
   return ok();
 }
 
@@ -402,9 +421,8 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
                         at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
     return rc;
   prof_mark(2, st);
-  lp::k_gather_rows<<<(S + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), tok_of, S, H,
-                                                 at<__nv_bfloat16>(ws, L.x_perm));
-  LP_CHECK_LAUNCH("k_gather_rows");
+  LP_CUDA(launch_pdl(lp::k_gather_rows, (S + 7) / 8, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
+                     static_cast<const int32_t*>(tok_of), S, H, at<__nv_bfloat16>(ws, L.x_perm)));
   if ((rc = launch_experts(at<void>(ws, L.x_perm), S, nullptr, S, w13, w2, H, I, E, max_n, offsets,
                            at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
@@ -451,5 +469,20 @@ int lp_profile_events(void* const* events, int n) {
   for (int i = 0; i < 5; ++i) g_prof[i] = (g_prof_n && i < n) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
   return ok();
 }
+
+#ifdef LP_TRACE
+// trace builds only (not part of include/lpmoe.h): read / reset the timestamps
+int lp_trace_fetch(unsigned long long* out, int n) {
+  if (n > 512) n = 512;
+  if (cudaMemcpyFromSymbol(out, lp::g_lp_trace, sizeof(unsigned long long) * n) != cudaSuccess) return LP_ECUDA;
+  return LP_OK;
+}
+int lp_trace_reset(void) {
+  unsigned long long init[512];
+  for (int i = 0; i < 512; ++i) init[i] = (i % 8 == 0 || i == 24 || i == 32 || i == 40) ? ~0ull : 0ull;
+  if (cudaMemcpyToSymbol(lp::g_lp_trace, init, sizeof(init)) != cudaSuccess) return LP_ECUDA;
+  return LP_OK;
+}
+#endif
 
 }  // extern "C"

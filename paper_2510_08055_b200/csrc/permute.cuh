@@ -16,6 +16,7 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
+#include "ptx.cuh"
 
 namespace lp {
 
@@ -30,6 +31,8 @@ __global__ void __launch_bounds__(32 * kHistWarps)
   extern __shared__ int32_t sh_hist[];
   const int wl = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int c = blockIdx.x * kHistWarps + wl;
+  pdl_trigger();
+  pdl_wait();
   int32_t* hist = sh_hist + wl * E;
   for (int e = lane; e < E; e += 32) hist[e] = 0;
   __syncwarp();
@@ -75,6 +78,9 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ int32_t s_til[256];
   __shared__ int32_t s_off[256];
   const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0) LP_TRACE_AT(true, 16);
   const int e_pad = (E + 31) & ~31;
   const int G = kScanThreads / e_pad;
   const int g = tid / e_pad;
@@ -93,6 +99,7 @@ __global__ void __launch_bounds__(kScanThreads)
     }
     __syncthreads();
   }
+  if (tid == 0) LP_TRACE_AT(true, 17);
   const int per = (nchunks + G - 1) / G;
   const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
   int sum = 0;
@@ -149,6 +156,7 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   for (int i = tid; i <= E; i += kScanThreads) sched[i] = 0u;
   __syncthreads();
+  if (tid == 0) LP_TRACE_AT(true, 18);
   // expert-contiguous slot of every routing entry and its inverse (slot -> token)
   for (int i0 = tid; i0 < S; i0 += 4 * kScanThreads) {
     int ex[4], rl[4];
@@ -169,6 +177,8 @@ __global__ void __launch_bounds__(kScanThreads)
       }
     }
   }
+  __syncthreads();
+  if (tid == 0) LP_TRACE_AT(true, 19);
 }
 
 // x_perm[slot] = x[tok_of[slot]] (standalone lp_moe_permute only; the fused
@@ -178,11 +188,15 @@ __global__ void __launch_bounds__(256)
                   __nv_bfloat16* __restrict__ x_perm) {
   const int slot = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) { LP_TRACE_MIN(24); }
   if (slot >= S) return;
   const int t = tok_of[slot];
   const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
   uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
   for (int v = lane; v < H / 8; v += 32) dst[v] = src[v];
+  if (lane == 0) LP_TRACE_MAX(25);
 }
 
 // y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]]   (fp32 accumulate in fixed j order, bf16 out)
@@ -195,6 +209,9 @@ __global__ void __launch_bounds__(kCombineThreads)
   __shared__ int s_slot[32];
   __shared__ float s_w[32];
   const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) LP_TRACE_MIN(40);
   if (threadIdx.x < topk) {
     s_slot[threadIdx.x] = slot_of[static_cast<size_t>(t) * topk + threadIdx.x];
     s_w[threadIdx.x] = w[static_cast<size_t>(t) * topk + threadIdx.x];
@@ -240,6 +257,7 @@ __global__ void __launch_bounds__(kCombineThreads)
     for (int q = 0; q < 4; ++q) o2[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
     reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * H)[v] = o;
   }
+  if (threadIdx.x == 0) LP_TRACE_MAX(41);
 }
 
 }  // namespace lp

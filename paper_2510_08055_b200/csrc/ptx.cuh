@@ -130,6 +130,21 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the layer is launched with programmatic stream serialization:
+// it may start while its predecessor is still running, triggers its own
+// dependents immediately, and must pdl_wait() before touching any global
+// buffer a predecessor reads or writes. Only the prologue (smem / TMEM /
+// barrier setup, descriptor and L2 prefetches of immutable weights) precedes it.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// L2 prefetch of one TMA box (no smem, no barrier): warms weights ahead of use.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -142,6 +157,35 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// ---------------------------------------------------------------- tracing (trace builds only)
+// Built with -DLP_TRACE into a separate library (tools/trace_layer.py); records
+// %globaltimer (ns) at phase boundaries into g_lp_trace[slot]. Zero cost otherwise.
+#ifdef LP_TRACE
+__device__ unsigned long long g_lp_trace[512];
+__device__ __forceinline__ void lp_trace(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_lp_trace[slot] = t;
+}
+__device__ __forceinline__ void lp_trace_min(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMin(&g_lp_trace[slot], t);
+}
+__device__ __forceinline__ void lp_trace_max(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_lp_trace[slot], t);
+}
+#define LP_TRACE_AT(cond, slot) do { if (cond) lp_trace(slot); } while (0)
+#define LP_TRACE_MIN(slot) lp_trace_min(slot)
+#define LP_TRACE_MAX(slot) lp_trace_max(slot)
+#else
+#define LP_TRACE_AT(cond, slot) do { } while (0)
+#define LP_TRACE_MIN(slot) do { } while (0)
+#define LP_TRACE_MAX(slot) do { } while (0)
+#endif
+
 __device__ __forceinline__ int warp_idx() { return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0); }
 __device__ __forceinline__ bool elect_lane0() { return (threadIdx.x & 31) == 0; }
 

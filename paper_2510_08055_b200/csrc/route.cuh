@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   const int lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * kRouterN;
   const int kblocks = p.H / 64;
+  const bool tr = blockIdx.x == 0;
+  if (threadIdx.x == 0) { LP_TRACE_AT(tr, 0); LP_TRACE_MIN(8); }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRouterStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -63,15 +65,20 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 32);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm_wr);
+    prefetch_tmap(&tm_x);
+  }
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  if (threadIdx.x == 0) LP_TRACE_AT(tr, 1);
 
   if (warp == 0) {
     if (lane == 0) {
-      prefetch_tmap(&tm_wr);
-      prefetch_tmap(&tm_x);
       const uint64_t pol = policy_evict_last();
       for (int i = 0; i < kblocks; ++i) {
         const int s = i % kRouterStages;
@@ -80,7 +87,9 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         for (int mt = 0; mt < p.mtiles; ++mt) tma_load_2d(sa + mt * 16384, &tm_wr, &full[s], i * 64, mt * 128, pol);
         tma_load_2d(sa + p.mtiles * 16384, &tm_x, &full[s], i * 64, t0, pol);
+        if (i == 0) LP_TRACE_AT(tr, 2);
       }
+      LP_TRACE_AT(tr, 3);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -112,6 +121,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
     mbar_wait(tfull, 0);
     tc_fence_after();
+    if (et == 0) LP_TRACE_AT(tr, 4);
     for (int mt = 0; mt < p.mtiles; ++mt) {
       uint32_t v[16];
       tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + mt * kRouterN, v);
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       }
     }
 
+    if (et == 0) LP_TRACE_AT(tr, 5);
     // ---------------- stable per-tile histogram + ranks: warp q owns tokens 4q..4q+3 ----------------
     for (int ee = lane; ee < e_pad; ee += 32) s_wh[q * e_pad + ee] = 0;
     __syncwarp();
@@ -224,6 +235,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 32);

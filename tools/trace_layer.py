@@ -1,0 +1,60 @@
+"""Phase timeline of one MoE-layer forward from the -DLP_TRACE build.
+
+    python -m paper_2510_08055_b200.build --trace
+    LP_T=576 python tools/trace_layer.py
+Prints %globaltimer deltas (ns) relative to the router's first CTA start.
+"""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["LPMOE_LIB"] = os.path.join(ROOT, "paper_2510_08055_b200", "_lib", "liblpmoe_trace.so")
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2510_08055_b200 import QWEN3_30B_A3B as s  # noqa: E402
+from paper_2510_08055_b200 import _native  # noqa: E402
+from paper_2510_08055_b200.moe import GpuMoE  # noqa: E402
+from paper_2510_08055_b200.synthetic import router_tokens, router_weight  # noqa: E402
+
+NAMES = {0: "router blk0 start", 1: "router blk0 setup done", 2: "router blk0 first TMA issued",
+         3: "router blk0 all TMA issued", 4: "router blk0 MMA done", 5: "router blk0 top-k done",
+         6: "router blk0 end", 8: "router first CTA start", 9: "router last CTA end",
+         16: "scan start", 17: "scan staged", 18: "scan offsets done", 19: "scan end",
+         24: "gather first", 25: "gather last", 32: "experts first CTA start", 33: "experts blk0 start",
+         34: "experts last CTA end", 35: "experts blk0 end", 40: "combine first", 41: "combine last"}
+
+
+def main():
+    T = int(os.environ.get("LP_T", "576"))
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    w13 = (torch.randn((s.num_experts, 2 * s.ffn, s.hidden), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    w2 = (torch.randn((s.num_experts, s.hidden, s.ffn), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    layer = GpuMoE(s, router_weight(s.num_experts, s.hidden, 0).to(dev), w13, w2)
+    x = router_tokens(T, s.hidden, 7).to(dev)
+    lib = _native.load()
+    lib.lp_trace_fetch.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    for _ in range(5):
+        layer(x)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        lib.lp_trace_reset()
+        torch.cuda.synchronize()
+        layer(x)
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * 512)()
+        lib.lp_trace_fetch(buf, 512)
+        t0 = buf[8]
+        print(f"--- T={T} rep {rep}")
+        for k in sorted(NAMES):
+            v = buf[k]
+            if v in (0, 2**64 - 1):
+                continue
+            print(f"{NAMES[k]:32s} {(v - t0) / 1000:9.2f} us")
+
+
+if __name__ == "__main__":
+    main()
