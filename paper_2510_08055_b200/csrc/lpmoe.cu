@@ -166,19 +166,33 @@ int sm_count() {
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its stream predecessor drains; kernels pdl_wait() before global I/O.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
+cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               int cluster, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int n = 1;
+  if (cluster > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    n = 2;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  return launch_pdl_cluster(kernel, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
 template <typename K>
@@ -189,6 +203,24 @@ int set_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------ stages
+// CTAs per router token tile: split H across a cluster while the grid is small.
+int router_cluster(int ntiles, int H) {
+  int cs = 1;
+  while (cs < 4 && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) cs *= 2;
+  return cs;
+}
+
+template <int NV>
+int launch_router_t(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
+                    cudaStream_t st) {
+  int rc;
+  const int smem = lp::router_smem_bytes(rp.mtiles);
+  if ((rc = set_smem(lp::k_router<NV>, smem))) return rc;
+  LP_CUDA(launch_pdl_cluster(lp::k_router<NV>, ntiles * rp.csize, lp::kRouterThreads, smem, st, rp.csize, tm_wr, tm_x,
+                             rp));
+  return LP_OK;
+}
+
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
                  void* ws, const Layout& L, cudaStream_t st) {
   int rc;
@@ -197,18 +229,26 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
   if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
   const int mtiles = (E + 127) / 128;
-  lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
+  const int cs = router_cluster(L.nchunks, H);
+  lp::RouterParams rp{T, H, E, topk, renorm, mtiles, cs, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
-  const int smem = lp::router_smem_bytes(mtiles);
-  if ((rc = set_smem(lp::k_router, smem))) return rc;
-  LP_CUDA(launch_pdl(lp::k_router, L.nchunks, lp::kRouterThreads, smem, st, tm_wr, tm_x, rp));
-  return LP_OK;
+  const int nv = ((E + 31) / 32 * 32) / 8;
+  switch (nv) {
+    case 4: return launch_router_t<4>(tm_wr, tm_x, rp, L.nchunks, st);
+    case 8: return launch_router_t<8>(tm_wr, tm_x, rp, L.nchunks, st);
+    case 12:
+    case 16: return launch_router_t<16>(tm_wr, tm_x, rp, L.nchunks, st);
+    default: return launch_router_t<32>(tm_wr, tm_x, rp, L.nchunks, st);
+  }
 }
 
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
-int launch_scan(const int32_t* ids, int T, int E, int topk, int32_t* counts, int32_t* offsets, int32_t* slot_of,
-                int32_t* tok_of, int32_t* chunk_hist, const int32_t* rank_local, int max_n, int32_t* tile_prefix,
-                int32_t* tile_rows, uint32_t* sched, cudaStream_t st) {
+// Scan (one CTA): per-tile bases, counts, offsets, expert tile schedule. Scatter
+// (one warp per routing entry): slot_of / tok_of and, if x_perm, the row copy.
+int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
+                        int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
+                        const int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows,
+                        uint32_t* sched, cudaStream_t st) {
   const int S = T * topk;
   const int nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
   const int n_hist = nchunks * E;
@@ -218,7 +258,10 @@ int launch_scan(const int32_t* ids, int T, int E, int topk, int32_t* counts, int
     if ((rc = set_smem(lp::k_scan, lp::kScanSmemInts * 4))) return rc;
   }
   LP_CUDA(launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts, offsets,
-                     tile_prefix, tile_rows, sched, ids, rank_local, S, topk, lp::kRouterN * topk, slot_of, tok_of));
+                     tile_prefix, tile_rows, sched));
+  LP_CUDA(launch_pdl(lp::k_scatter, (S + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
+                     static_cast<const int32_t*>(offsets), static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
+                     lp::kRouterN * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
   return LP_OK;
 }
 
@@ -342,15 +385,10 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   lp::k_chunk_hist<<<(L.nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
                      lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, T * topk, E, chunk, chunk_hist, rank_local);
   LP_CHECK_LAUNCH("k_chunk_hist");
-  if ((rc = launch_scan(ids, T, E, topk, counts, offsets, slot_of, tok_of, chunk_hist, rank_local, max_n,
-                        at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm, chunk_hist,
+                                rank_local, max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                at<uint32_t>(ws, L.sched), st)))
     return rc;
-  if (x_perm) {
-    const int S = T * topk;
-    lp::k_gather_rows<<<(S + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), tok_of, S, H,
-                                                   static_cast<__nv_bfloat16*>(x_perm));
-    LP_CHECK_LAUNCH("k_gather_rows");
-  }
   return ok();
 }
 
@@ -416,13 +454,12 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
   prof_mark(1, st);
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
-  if ((rc = launch_scan(ids, T, E, topk, counts, offsets, slot_of, tok_of, at<int32_t>(ws, L.chunk_hist),
-                        at<int32_t>(ws, L.rank_local), max_n, at<int32_t>(ws, L.tile_prefix),
-                        at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), st)))
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, at<void>(ws, L.x_perm),
+                                at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
+                                at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                at<uint32_t>(ws, L.sched), st)))
     return rc;
   prof_mark(2, st);
-  LP_CUDA(launch_pdl(lp::k_gather_rows, (S + 7) / 8, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
-                     static_cast<const int32_t*>(tok_of), S, H, at<__nv_bfloat16>(ws, L.x_perm)));
   if ((rc = launch_experts(at<void>(ws, L.x_perm), S, nullptr, S, w13, w2, H, I, E, max_n, offsets,
                            at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),

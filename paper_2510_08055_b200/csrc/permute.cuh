@@ -70,13 +70,11 @@ constexpr int kScanSmemInts = 24576;  // 96 KiB
 __global__ void __launch_bounds__(kScanThreads)
     k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n, int32_t* __restrict__ counts,
            int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
-           uint32_t* __restrict__ sched, const int32_t* __restrict__ ids, const int32_t* __restrict__ rank_local,
-           int S, int topk, int chunk, int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of) {
+           uint32_t* __restrict__ sched) {
   extern __shared__ int32_t s_hist[];
   __shared__ int32_t s_part[kScanThreads];
   __shared__ int32_t s_cnt[256];
   __shared__ int32_t s_til[256];
-  __shared__ int32_t s_off[256];
   const int tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
@@ -127,58 +125,75 @@ __global__ void __launch_bounds__(kScanThreads)
       run += v;
     }
   }
-  // offsets / tile schedule over experts (e_pad <= 256 threads)
+  // offsets / tile schedule over experts: warp-shuffle scans (e_pad <= 256 -> <= 8 warps)
   int cnt = 0, ntiles = 0;
   if (tid < e_pad) {
     cnt = s_cnt[tid];
     ntiles = (cnt > 0) ? (cnt + max_n - 1) / max_n : 0;
-    s_til[tid] = ntiles;
     if (tid < E) counts[tid] = cnt;
+    int a = cnt, b = ntiles;
+    const int lane = tid & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ua = __shfl_up_sync(0xffffffffu, a, o);
+      const int ub = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) { a += ua; b += ub; }
+    }
+    s_cnt[tid] = a;  // inclusive within the warp
+    s_til[tid] = b;
   }
   __syncthreads();
-  for (int o = 1; o < e_pad; o <<= 1) {
-    int a = 0, b = 0;
-    if (tid < e_pad && tid >= o) { a = s_cnt[tid - o]; b = s_til[tid - o]; }
-    __syncthreads();
-    if (tid < e_pad) { s_cnt[tid] += a; s_til[tid] += b; }
-    __syncthreads();
-  }
-  if (tid < E) {
-    offsets[tid] = s_cnt[tid] - cnt;
-    s_off[tid] = s_cnt[tid] - cnt;
-    tile_prefix[tid] = s_til[tid] - ntiles;
-    const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
-    tile_rows[tid] = min(max_n, (rows + 15) & ~15);
-    if (tid == E - 1) {
-      offsets[E] = s_cnt[tid];
-      tile_prefix[E] = s_til[tid];
-    }
-  }
-  for (int i = tid; i <= E; i += kScanThreads) sched[i] = 0u;
-  __syncthreads();
-  if (tid == 0) LP_TRACE_AT(true, 18);
-  // expert-contiguous slot of every routing entry and its inverse (slot -> token)
-  for (int i0 = tid; i0 < S; i0 += 4 * kScanThreads) {
-    int ex[4], rl[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * kScanThreads;
-      ex[u] = (i < S) ? __ldcg(ids + i) : -1;
-      rl[u] = (i < S) ? __ldcg(rank_local + i) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * kScanThreads;
-      if (ex[u] >= 0) {
-        const size_t at = static_cast<size_t>(i / chunk) * E + ex[u];
-        const int slot = s_off[ex[u]] + (staged ? hist[at] : __ldcg(hist + at)) + rl[u];
-        slot_of[i] = slot;
-        tok_of[slot] = i / topk;
+  if (tid < e_pad) {
+    int wa = 0, wb = 0;
+    for (int w = 0; w < (tid >> 5); ++w) { wa += s_cnt[w * 32 + 31]; wb += s_til[w * 32 + 31]; }
+    const int inc_a = s_cnt[tid] + wa, inc_b = s_til[tid] + wb;
+    if (tid < E) {
+      offsets[tid] = inc_a - cnt;
+      tile_prefix[tid] = inc_b - ntiles;
+      const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
+      tile_rows[tid] = min(max_n, (rows + 15) & ~15);
+      if (tid == E - 1) {
+        offsets[E] = inc_a;
+        tile_prefix[E] = inc_b;
       }
     }
   }
+  for (int i = tid; i <= E; i += kScanThreads) sched[i] = 0u;
+  if (!staged) return;
+  // staged path: the per-tile bases live in smem; publish them for the scatter
   __syncthreads();
-  if (tid == 0) LP_TRACE_AT(true, 19);
+  for (int i = tid; i < n_hist; i += kScanThreads) chunk_hist[i] = s_hist[i];
+  if (tid == 0) LP_TRACE_AT(true, 18);
+}
+
+// One warp per routing entry i = t*topk + j: its expert-contiguous slot, the
+// inverse map, and (optionally) the copy of token row t into x_perm[slot].
+__global__ void __launch_bounds__(256)
+    k_scatter(const int32_t* __restrict__ ids, const int32_t* __restrict__ chunk_base,
+              const int32_t* __restrict__ rank_local, const int32_t* __restrict__ offsets,
+              const __nv_bfloat16* __restrict__ x, int S, int E, int topk, int H, int chunk,
+              int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of, __nv_bfloat16* __restrict__ x_perm) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) LP_TRACE_MIN(24);
+  if (i >= S) return;
+  const int e = __ldcg(ids + i);
+  const int t = i / topk;
+  const int slot = __ldcg(offsets + e) + __ldcg(chunk_base + static_cast<size_t>(i / chunk) * E + e) +
+                   __ldcg(rank_local + i);
+  if (lane == 0) {
+    slot_of[i] = slot;
+    tok_of[slot] = t;
+  }
+  if (x_perm != nullptr) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+    uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
+    const int nv = H / 8;
+    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+  }
+  if (lane == 0) LP_TRACE_MAX(25);
 }
 
 // x_perm[slot] = x[tok_of[slot]] (standalone lp_moe_permute only; the fused

@@ -1,5 +1,5 @@
 // K1: router logits (tcgen05) + softmax / top-k gating + per-tile expert
-// histogram, in ONE launch, one CTA per 16-token tile.
+// histogram, in ONE launch.
 //
 // Semantics follow HF transformers 5.5 `Qwen3MoeTopKRouter.forward`
 // (modeling_qwen3_moe.py:260-270): logits = x . Wr^T accumulated in fp32,
@@ -8,39 +8,84 @@
 // (logit desc, expert index asc) on both the GPU and the oracle.
 //
 // Tiling (swap-AB): M = 128 expert rows of Wr per m-tile (E <= 256 -> up to
-// two m-tiles accumulated side by side in TMEM), N = 16 tokens, K = H streamed
-// through a 6-deep TMA ring (Wr, 0.5 MB for Qwen, stays L2-resident across
-// CTAs). No split-K: every CTA owns complete logits, so the epilogue goes
-// TMEM -> smem -> top-k without any cross-CTA step. Epilogue (4 warps):
+// two m-tiles accumulated side by side in TMEM), N = 16 tokens per tile.
+// Small batches are latency-bound on streaming Wr (0.5 MB for Qwen, L2
+// resident), so each token tile is owned by a thread-block CLUSTER of `csize`
+// CTAs that split K = H: every CTA streams 1/csize of Wr through a 6-deep TMA
+// ring, parks its fp32 partial logits in its own smem, and the leader CTA sums
+// the partials over DSMEM in fixed rank order (deterministic, no global round
+// trip). The leader's 4 epilogue warps then run
 //   * softmax + top-k with 8 lanes per token (all 16 tokens concurrently);
-//   * stable per-tile expert histogram + in-tile ranks of the routing entries
-//     (match_any within a warp, exclusive scan across the 4 warps) that the
-//     permutation (permute.cuh) turns into expert-contiguous slots.
+//   * the stable per-tile expert histogram + in-tile ranks of the routing
+//     entries (match_any within a warp, exclusive scan across the 4 warps)
+//     that the permutation (permute.cuh) turns into expert-contiguous slots.
 #pragma once
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 
 namespace lp {
 
-constexpr int kRouterN = 16;        // tokens per router tile (= permutation chunk)
+constexpr int kRouterN = 16;         // tokens per router tile (= permutation chunk)
 constexpr int kRouterStages = 6;
-constexpr int kRouterThreads = 192; // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
+constexpr int kRouterThreads = 192;  // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
 constexpr int kRouterBBytes = kRouterN * 128;
-constexpr int kRouterMaxStage = 2 * 16384 + kRouterBBytes;
 __host__ __device__ constexpr int router_smem_bytes(int mtiles) {
   return 1024 + kRouterStages * (mtiles * 16384 + kRouterBBytes) + 256;
 }
-constexpr int kRouterVals = 32;     // logits per lane in the top-k (E_pad / 8 <= 32)
 
 struct RouterParams {
   int T, H, E, topk, renorm;
   int mtiles;           // ceil(E / 128)
+  int csize;            // CTAs per token tile (cluster size, splits H)
   int32_t* ids;         // [T, topk]
   float* w;             // [T, topk]
   int32_t* tile_hist;   // [ntiles, E] per-tile expert counts
   int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its tile
 };
 
+// Softmax + top-k of one token held by 8 consecutive lanes (lane `sub` owns
+// experts sub, sub+8, ...). Writes the k ids / probabilities to smem.
+template <int NV>
+__device__ __forceinline__ void topk_8lanes(const float* row, int E, int topk, int sub, int32_t* out_ids,
+                                            float* out_p, float& psum) {
+  float l[NV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int ex = sub + 8 * j;
+    l[j] = (ex < E) ? row[ex] : -INFINITY;
+    m = fmaxf(m, l[j]);
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float ssum = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  uint32_t taken = 0;
+  psum = 0.f;
+  for (int r = 0; r < topk; ++r) {
+    float bv = -INFINITY;
+    int bj = -1;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)  // ascending expert index: the first maximum wins ties
+      if (!((taken >> j) & 1u) && l[j] > bv) { bv = l[j]; bj = j; }
+    int bi = bj >= 0 ? sub + 8 * bj : 0x7fffffff;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if ((bi & 7) == sub) taken |= 1u << (bi >> 3);
+    const float pr = expf(bv - m) / ssum;
+    psum += pr;
+    if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
+  }
+}
+
+template <int NV>
 __global__ void __launch_bounds__(kRouterThreads, 1)
     k_router(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const RouterParams p) {
@@ -54,8 +99,11 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * kRouterN;
-  const int kblocks = p.H / 64;
+  const int cr = p.csize > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int tile = blockIdx.x / p.csize;
+  const int t0 = tile * kRouterN;
+  const int kb_per = (p.H / 64) / p.csize;
+  const int kb0 = cr * kb_per;
   const bool tr = blockIdx.x == 0;
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 0); LP_TRACE_MIN(8); }
 
@@ -63,12 +111,10 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     for (int s = 0; s < kRouterStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 32);
-  if (threadIdx.x == 0) {
     prefetch_tmap(&tm_wr);
     prefetch_tmap(&tm_x);
   }
+  if (warp == 1) tmem_alloc(tmem_slot, 32);
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
@@ -77,24 +123,31 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   pdl_wait();
   if (threadIdx.x == 0) LP_TRACE_AT(tr, 1);
 
+  const int e_pad = (p.E + 31) & ~31;
+  float* s_part = reinterpret_cast<float*>(smem);             // [kRouterN][e_pad] this CTA's partial logits
+  float* s_logit = s_part + kRouterN * 256;                    // [kRouterN][e_pad] full logits (leader)
+  int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
+  float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
+  int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
+
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();
-      for (int i = 0; i < kblocks; ++i) {
+      for (int i = 0; i < kb_per; ++i) {
         const int s = i % kRouterStages;
         mbar_wait(&empty[s], ((i / kRouterStages) & 1) ^ 1);
         uint8_t* sa = smem + s * stage_bytes;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        for (int mt = 0; mt < p.mtiles; ++mt) tma_load_2d(sa + mt * 16384, &tm_wr, &full[s], i * 64, mt * 128, pol);
-        tma_load_2d(sa + p.mtiles * 16384, &tm_x, &full[s], i * 64, t0, pol);
-        if (i == 0) LP_TRACE_AT(tr, 2);
+        for (int mt = 0; mt < p.mtiles; ++mt)
+          tma_load_2d(sa + mt * 16384, &tm_wr, &full[s], (kb0 + i) * 64, mt * 128, pol);
+        tma_load_2d(sa + p.mtiles * 16384, &tm_x, &full[s], (kb0 + i) * 64, t0, pol);
       }
       LP_TRACE_AT(tr, 3);
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, kRouterN);
-      for (int i = 0; i < kblocks; ++i) {
+      for (int i = 0; i < kb_per; ++i) {
         const int s = i % kRouterStages;
         mbar_wait(&full[s], (i / kRouterStages) & 1);
         tc_fence_after();
@@ -111,17 +164,12 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       mma_commit(tfull);
     }
   } else {
-    // ========================= epilogue: 4 warps, 128 threads =========================
+    // TMEM -> smem (the ring is drained once tfull fires: every MMA has read its stage)
     const int q = warp & 3;
-    const int et = threadIdx.x - 64;  // 0..127
-    const int e_pad = (p.E + 31) & ~31;
-    float* s_logit = reinterpret_cast<float*>(smem);                 // [kRouterN][e_pad] (ring is drained)
-    int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
-    float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
-    int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
     mbar_wait(tfull, 0);
     tc_fence_after();
-    if (et == 0) LP_TRACE_AT(tr, 4);
+    if (threadIdx.x == 64) LP_TRACE_AT(tr, 4);
+    float* dst = p.csize > 1 ? s_part : s_logit;
     for (int mt = 0; mt < p.mtiles; ++mt) {
       uint32_t v[16];
       tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + mt * kRouterN, v);
@@ -129,54 +177,42 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       const int e = mt * 128 + 32 * q + lane;
       if (e < e_pad) {
 #pragma unroll
-        for (int i = 0; i < kRouterN; ++i) s_logit[i * e_pad + e] = __uint_as_float(v[i]);
+        for (int i = 0; i < kRouterN; ++i) dst[i * e_pad + e] = __uint_as_float(v[i]);
       }
     }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (p.csize > 1) {
+    cluster_sync();  // every CTA's partial logits are now readable over DSMEM
+    if (cr == 0 && warp >= 2) {
+      // leader: s_logit = sum_r partial_r in rank order (float4 over experts)
+      const int et = threadIdx.x - 64;
+      const int nq = kRouterN * (e_pad / 4);
+      for (int idx = et; idx < nq; idx += 128) {
+        const int off = idx * 4;
+        float4 acc = *reinterpret_cast<const float4*>(s_part + off);
+        const uint32_t la = smem_u32(s_part + off);
+        for (int r = 1; r < p.csize; ++r) {
+          const float4 v = ld_dsmem_f4(mapa_shared(la, r));
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(s_logit + off) = acc;
+      }
+    }
+    cluster_sync();  // partials consumed: non-leaders may leave
+  }
+  if (cr == 0 && warp >= 2) {
+    const int q = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
     named_bar_sync(1, 128);
-
     // ---------------- softmax + top-k: 8 lanes per token ----------------
     {
-      const int g = et >> 3;   // token within the tile
-      const int sub = et & 7;  // lane within the token group
+      const int g = et >> 3;
+      const int sub = et & 7;
       const int t = t0 + g;
-      const int nv = e_pad >> 3;
-      float l[kRouterVals];
-      float m = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < kRouterVals; ++j) {
-        const int ex = sub + 8 * j;
-        l[j] = (j < nv && ex < p.E) ? s_logit[g * e_pad + ex] : -INFINITY;
-        m = fmaxf(m, l[j]);
-      }
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      float ssum = 0.f;
-#pragma unroll
-      for (int j = 0; j < kRouterVals; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
-      float psum = 0.f;
-      for (int r = 0; r < p.topk; ++r) {
-        float bv = -INFINITY;
-        int bi = 0x7fffffff;
-#pragma unroll
-        for (int j = 0; j < kRouterVals; ++j) {
-          const int ex = sub + 8 * j;
-          if (l[j] > bv) { bv = l[j]; bi = ex; }  // ascending ex: first max wins ties
-        }
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-#pragma unroll
-        for (int j = 0; j < kRouterVals; ++j)
-          if (sub + 8 * j == bi) l[j] = -INFINITY;
-        const float pr = expf(bv - m) / ssum;
-        psum += pr;
-        if (sub == 0) { s_ids[g * 32 + r] = bi; s_p[g * 32 + r] = pr; }
-      }
+      float psum;
+      topk_8lanes<NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
       __syncwarp();
       if (t < p.T) {
         for (int r = sub; r < p.topk; r += 8) {
@@ -185,7 +221,6 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         }
       }
     }
-
     if (et == 0) LP_TRACE_AT(tr, 5);
     // ---------------- stable per-tile histogram + ranks: warp q owns tokens 4q..4q+3 ----------------
     for (int ee = lane; ee < e_pad; ee += 32) s_wh[q * e_pad + ee] = 0;
@@ -223,7 +258,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         s_wh[w4 * e_pad + ee] = run;
         run += c;
       }
-      if (ee < p.E) p.tile_hist[static_cast<size_t>(blockIdx.x) * p.E + ee] = run;
+      if (ee < p.E) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = run;
     }
     named_bar_sync(1, 128);
 #pragma unroll

@@ -22,8 +22,8 @@ from paper_2510_08055_b200.synthetic import router_tokens, router_weight  # noqa
 NAMES = {0: "router blk0 start", 1: "router blk0 setup done", 2: "router blk0 first TMA issued",
          3: "router blk0 all TMA issued", 4: "router blk0 MMA done", 5: "router blk0 top-k done",
          6: "router blk0 end", 8: "router first CTA start", 9: "router last CTA end",
-         16: "scan start", 17: "scan staged", 18: "scan offsets done", 19: "scan end",
-         24: "gather first", 25: "gather last", 32: "experts first CTA start", 33: "experts blk0 start",
+         16: "scan start", 17: "scan staged", 18: "scan end (staged)",
+         24: "scatter first", 25: "scatter last", 32: "experts first CTA start", 33: "experts blk0 start",
          34: "experts last CTA end", 35: "experts blk0 end", 40: "combine first", 41: "combine last"}
 
 
