@@ -14,8 +14,11 @@
 //   UP  (e, mt, nt): 128 gate rows + the matching 128 up rows, K = H.
 //                    Gate and up accumulate into separate TMEM column ranges
 //                    of the same lanes, so SiLU(g)*u is a per-thread epilogue.
-//   DN  (e, mt, nt): 128 rows of W2 (output features), K = I, waits until all
-//                    UP items of expert e have published their act rows.
+//   DN  (e, mt, nt): 256 rows of W2 (output features) as two 128-row tiles
+//                    accumulated side by side (same smem/TMEM shape as UP, so
+//                    both phases keep 2 weight tiles in flight per stage),
+//                    K = I, waits until all UP items of expert e have
+//                    published their act rows.
 // Items are claimed dynamically (global atomic) by 1 CTA/SM; all UP items
 // precede all DN items, so a DN wait can only target items already claimed
 // by running CTAs (deadlock-free without co-residency guarantees).
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int mt_up = p.I / kTileM;
-  const int mt_dn = p.H / kTileM;
+  const int mt_dn = (p.H + 2 * kTileM - 1) / (2 * kTileM);
   const int total_tiles = s_tp[E];
   const int n_up = mt_up * total_tiles;
   const int n_items = (mt_up + mt_dn) * total_tiles;
@@ -143,6 +146,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     int stage = 0; uint32_t phase = 0;
     int r = 0; uint32_t rph = 0;
     bool first = true;
+#ifdef LP_TRACE
+    int n_claimed = 0;
+#endif
     while (true) {
       int it = 0;  // first item static (matches the L2 prefetch), then dynamic
       if (lane == 0) it = first ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x + atomicAdd(&p.sched[0], 1u));
@@ -169,13 +175,20 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const int ts = s_ts[e];
         const int row0 = s_off[e] + nt * ts;
         const int nvalid = min(ts, n_e - nt * ts);
-        info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * kTileM, row0, nvalid);
+        info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * (up ? kTileM : 2 * kTileM), row0, nvalid);
         need = mt_up * nt_e;
       }
       if (lane == 0) {
         mbar_wait(&sempty[r], rph ^ 1);
         ring[r] = info;
         mbar_arrive(&sfull[r]);
+#ifdef LP_TRACE
+        if (blockIdx.x < 4 && n_claimed < 30) {
+          lp_trace(64 + blockIdx.x * 32 + n_claimed);
+          g_lp_trace[192 + blockIdx.x * 32 + n_claimed] = static_cast<unsigned long long>(it);
+        }
+        ++n_claimed;
+#endif
       }
       if (++r == kRing) { r = 0; rph ^= 1; }
       const int kind = info.x & 0xff;
@@ -197,8 +210,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           fence_proxy_async_global();
         }
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
-        const uint32_t bytes = up ? 2 * kATileBytes + (GATHER ? nmma * 128 : nbox * kBoxRows * 128)
-                                  : kATileBytes + nbox * kBoxRows * 128;
+        const bool two = up || m0 + kTileM < p.H;  // second A tile (up rows / upper W2 rows)
+        const uint32_t bytes = (two ? 2 : 1) * kATileBytes +
+                               (GATHER && up ? nmma * 128 : nbox * kBoxRows * 128);
         const int arow = up ? e * 2 * p.I + m0 : e * p.H + m0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -219,6 +233,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
             }
           } else {
             tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, arow, pol_w);
+            if (two) tma_load_2d(sa + kATileBytes, &tm_w2, &full[stage], kb * kTileK, arow + kTileM, pol_w);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(sb + b * kBoxRows * 128, &tm_act, &full[stage], kb * kTileK, row0 + b * kBoxRows, pol_a);
           }
@@ -241,6 +256,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const int kind = info.x & 0xff;
         if (kind == kItemEnd) break;
         const bool up = kind == kItemUp;
+        const bool two = up || info.y + kTileM < p.H;
         const int nmma = (info.w + 15) & ~15;
         const uint32_t idesc = idesc_bf16_f32(kTileM, nmma);
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
@@ -259,7 +275,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           for (int k = 0; k < kTileK / 16; ++k) {
             const uint32_t accum = (kb | k) != 0;
             mma_bf16(d_gate, a0 + 2 * k, b0 + 2 * k, idesc, accum);
-            if (up) mma_bf16(d_up, a1 + 2 * k, b0 + 2 * k, idesc, accum);
+            if (two) mma_bf16(d_up, a1 + 2 * k, b0 + 2 * k, idesc, accum);
           }
           mma_commit(&empty[stage]);
           if (++stage == S_) { stage = 0; phase ^= 1; }
@@ -268,6 +284,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         if (++acc == A_) { acc = 0; aph ^= 1; }
       }
     }
+    __syncwarp();
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs -> global =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -301,15 +318,20 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           }
         }
       } else {
+        const bool two = m0 + kTileM < p.H;
         __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
         for (int c = 0; c < nchunks; ++c) {
-          uint32_t v[16];
+          uint32_t v[16], v2[16];
           tmem_ld16(t_gate + c * 16, v);
+          if (two) tmem_ld16(t_gate + MAX_N + c * 16, v2);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int n = c * 16 + i;
-            if (n < nvalid) dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
+            if (n < nvalid) {
+              dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
+              if (two) dst[static_cast<size_t>(n) * p.H + kTileM] = __float2bfloat16_rn(__uint_as_float(v2[i]));
+            }
           }
         }
       }

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -77,13 +78,24 @@ constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E
 struct Layout {
   size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
   size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
+  int csize;         // router cluster size
+  int chunk_tokens;  // tokens per permutation chunk (= kRouterN / csize)
   int nchunks;
 };
+
+// CTAs per router token tile: split H across a cluster while the grid is small.
+int router_cluster(int ntiles, int H) {
+  int cs = 1;
+  while (cs < 4 && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) cs *= 2;
+  return cs;
+}
 
 Layout make_layout(int T, int H, int I, int E, int topk) {
   Layout L{};
   const size_t S = static_cast<size_t>(T) * topk;
-  L.nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
+  L.csize = router_cluster((T + lp::kRouterN - 1) / lp::kRouterN, H);
+  L.chunk_tokens = lp::kRouterN / L.csize;
+  L.nchunks = (T + L.chunk_tokens - 1) / L.chunk_tokens;
   size_t o = kHeaderBytes;
   auto take = [&](size_t bytes) {
     const size_t at = o;
@@ -203,22 +215,25 @@ int set_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------ stages
-// CTAs per router token tile: split H across a cluster while the grid is small.
-int router_cluster(int ntiles, int H) {
-  int cs = 1;
-  while (cs < 4 && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) cs *= 2;
-  return cs;
-}
-
-template <int NV>
+template <int CS, int NV>
 int launch_router_t(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
                     cudaStream_t st) {
   int rc;
   const int smem = lp::router_smem_bytes(rp.mtiles);
-  if ((rc = set_smem(lp::k_router<NV>, smem))) return rc;
-  LP_CUDA(launch_pdl_cluster(lp::k_router<NV>, ntiles * rp.csize, lp::kRouterThreads, smem, st, rp.csize, tm_wr, tm_x,
-                             rp));
+  if ((rc = set_smem(lp::k_router<CS, NV>, smem))) return rc;
+  LP_CUDA(launch_pdl_cluster(lp::k_router<CS, NV>, ntiles * CS, lp::kRouterThreads, smem, st, CS, tm_wr, tm_x, rp));
   return LP_OK;
+}
+
+template <int CS>
+int launch_router_cs(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
+                     int e_pad, cudaStream_t st) {
+  constexpr int LPT = 8 * CS;  // lanes per token
+  const int nv = (e_pad + LPT - 1) / LPT;
+  if (nv <= 4) return launch_router_t<CS, 4>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 8) return launch_router_t<CS, 8>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 16) return launch_router_t<CS, 16>(tm_wr, tm_x, rp, ntiles, st);
+  return launch_router_t<CS, 32>(tm_wr, tm_x, rp, ntiles, st);
 }
 
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
@@ -229,28 +244,26 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
   if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
   const int mtiles = (E + 127) / 128;
-  const int cs = router_cluster(L.nchunks, H);
-  lp::RouterParams rp{T, H, E, topk, renorm, mtiles, cs, ids, w, at<int32_t>(ws, L.chunk_hist),
+  lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
-  const int nv = ((E + 31) / 32 * 32) / 8;
-  switch (nv) {
-    case 4: return launch_router_t<4>(tm_wr, tm_x, rp, L.nchunks, st);
-    case 8: return launch_router_t<8>(tm_wr, tm_x, rp, L.nchunks, st);
-    case 12:
-    case 16: return launch_router_t<16>(tm_wr, tm_x, rp, L.nchunks, st);
-    default: return launch_router_t<32>(tm_wr, tm_x, rp, L.nchunks, st);
+  const int ntiles = (T + lp::kRouterN - 1) / lp::kRouterN;
+  const int e_pad = (E + 31) / 32 * 32;
+  switch (L.csize) {
+    case 4: return launch_router_cs<4>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    case 2: return launch_router_cs<2>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    default: return launch_router_cs<1>(tm_wr, tm_x, rp, ntiles, e_pad, st);
   }
 }
 
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
 // Scan (one CTA): per-tile bases, counts, offsets, expert tile schedule. Scatter
 // (one warp per routing entry): slot_of / tok_of and, if x_perm, the row copy.
-int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int32_t* counts,
-                        int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm, int32_t* chunk_hist,
-                        const int32_t* rank_local, int max_n, int32_t* tile_prefix, int32_t* tile_rows,
-                        uint32_t* sched, cudaStream_t st) {
+int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int chunk_tokens,
+                        int32_t* counts, int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm,
+                        int32_t* chunk_hist, const int32_t* rank_local, int max_n, int32_t* tile_prefix,
+                        int32_t* tile_rows, uint32_t* sched, cudaStream_t st) {
   const int S = T * topk;
-  const int nchunks = (T + lp::kRouterN - 1) / lp::kRouterN;
+  const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
   const int n_hist = nchunks * E;
   const int smem = n_hist <= lp::kScanSmemInts ? n_hist * 4 : 0;
   if (smem > 48 * 1024) {
@@ -261,7 +274,7 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
                      tile_prefix, tile_rows, sched));
   LP_CUDA(launch_pdl(lp::k_scatter, (S + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
                      static_cast<const int32_t*>(offsets), static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
-                     lp::kRouterN * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
+                     chunk_tokens * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
   return LP_OK;
 }
 
@@ -282,7 +295,15 @@ int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, c
   return LP_OK;
 }
 
-constexpr int kPrefetchKBlocks = 16;  // 2 x 16 x 16 KiB = 0.5 MiB of W13 per CTA warmed before pdl_wait
+// k-blocks of the first item's W13 warmed in L2 before pdl_wait (2 x 16 KiB each);
+// tuning knob LPMOE_PREFETCH_KB (default 16 -> 0.5 MiB per CTA).
+int prefetch_kblocks() {
+  static const int v = [] {
+    const char* s = getenv("LPMOE_PREFETCH_KB");
+    return s ? atoi(s) : 16;
+  }();
+  return v;
+}
 
 // src: [src_rows, H] token rows; slot s reads row tok_of[s] (tok_of == nullptr: row s).
 int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, const void* w13, const void* w2,
@@ -290,7 +311,7 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
                    const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st) {
   lp::ExpertsParams p{H,       I,           E,        tok_of, offsets, tile_prefix, tile_rows,
                       static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                      kPrefetchKBlocks};
+                      prefetch_kblocks()};
   if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
     switch (max_n) {
       case 64: return launch_experts_t<64, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
@@ -381,11 +402,12 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   const int max_n = pick_max_n(T * topk, E);
   int32_t* chunk_hist = at<int32_t>(ws, L.chunk_hist);
   int32_t* rank_local = at<int32_t>(ws, L.rank_local);
-  const int chunk = lp::kRouterN * topk;
+  const int chunk = L.chunk_tokens * topk;
   lp::k_chunk_hist<<<(L.nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
                      lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, T * topk, E, chunk, chunk_hist, rank_local);
   LP_CHECK_LAUNCH("k_chunk_hist");
-  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, x_perm, chunk_hist,
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of, x_perm,
+                                chunk_hist,
                                 rank_local, max_n, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
                                 at<uint32_t>(ws, L.sched), st)))
     return rc;
@@ -454,7 +476,8 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
   prof_mark(1, st);
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
-  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, counts, offsets, slot_of, tok_of, at<void>(ws, L.x_perm),
+  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
+                                at<void>(ws, L.x_perm),
                                 at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
                                 at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
                                 at<uint32_t>(ws, L.sched), st)))

@@ -12,20 +12,21 @@
 // Small batches are latency-bound on streaming Wr (0.5 MB for Qwen, L2
 // resident), so each token tile is owned by a thread-block CLUSTER of `csize`
 // CTAs that split K = H: every CTA streams 1/csize of Wr through a 6-deep TMA
-// ring, parks its fp32 partial logits in its own smem, and the leader CTA sums
-// the partials over DSMEM in fixed rank order (deterministic, no global round
-// trip). The leader's 4 epilogue warps then run
-//   * softmax + top-k with 8 lanes per token (all 16 tokens concurrently);
-//   * the stable per-tile expert histogram + in-tile ranks of the routing
-//     entries (match_any within a warp, exclusive scan across the 4 warps)
-//     that the permutation (permute.cuh) turns into expert-contiguous slots.
+// ring and parks its fp32 partial logits in its own smem. CTA r of the
+// cluster then owns tokens [r*16/csize, (r+1)*16/csize) of the tile: it sums
+// those rows of every CTA's partials over DSMEM in fixed rank order
+// (deterministic, no global round trip) and its 4 epilogue warps run
+//   * softmax + top-k with 8*csize lanes per token (all tokens concurrently);
+//   * the stable expert histogram of its token chunk + in-chunk ranks of the
+//     routing entries (match_any within a warp, exclusive scan across the 4
+//     warps), which the permutation (permute.cuh) turns into slots.
 #pragma once
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 
 namespace lp {
 
-constexpr int kRouterN = 16;         // tokens per router tile (= permutation chunk)
+constexpr int kRouterN = 16;         // tokens per router tile; a chunk is kRouterN / csize tokens
 constexpr int kRouterStages = 6;
 constexpr int kRouterThreads = 192;  // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
 constexpr int kRouterBBytes = kRouterN * 128;
@@ -36,33 +37,32 @@ __host__ __device__ constexpr int router_smem_bytes(int mtiles) {
 struct RouterParams {
   int T, H, E, topk, renorm;
   int mtiles;           // ceil(E / 128)
-  int csize;            // CTAs per token tile (cluster size, splits H)
   int32_t* ids;         // [T, topk]
   float* w;             // [T, topk]
-  int32_t* tile_hist;   // [ntiles, E] per-tile expert counts
-  int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its tile
+  int32_t* tile_hist;   // [nchunks, E] per-chunk expert counts (chunk = kRouterN/CS tokens)
+  int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its chunk
 };
 
-// Softmax + top-k of one token held by 8 consecutive lanes (lane `sub` owns
-// experts sub, sub+8, ...). Writes the k ids / probabilities to smem.
-template <int NV>
-__device__ __forceinline__ void topk_8lanes(const float* row, int E, int topk, int sub, int32_t* out_ids,
-                                            float* out_p, float& psum) {
+// Softmax + top-k of one token held by LPT consecutive lanes (lane `sub` owns
+// experts sub, sub+LPT, ...). Writes the k ids / probabilities to smem.
+template <int LPT, int NV>
+__device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, int sub, int32_t* out_ids, float* out_p,
+                                           float& psum) {
   float l[NV];
   float m = -INFINITY;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const int ex = sub + 8 * j;
+    const int ex = sub + LPT * j;
     l[j] = (ex < E) ? row[ex] : -INFINITY;
     m = fmaxf(m, l[j]);
   }
 #pragma unroll
-  for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 1; o < LPT; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float ssum = 0.f;
 #pragma unroll
   for (int j = 0; j < NV; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
 #pragma unroll
-  for (int o = 1; o < 8; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  for (int o = 1; o < LPT; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
   uint32_t taken = 0;
   psum = 0.f;
   for (int r = 0; r < topk; ++r) {
@@ -71,21 +71,22 @@ __device__ __forceinline__ void topk_8lanes(const float* row, int E, int topk, i
 #pragma unroll
     for (int j = 0; j < NV; ++j)  // ascending expert index: the first maximum wins ties
       if (!((taken >> j) & 1u) && l[j] > bv) { bv = l[j]; bj = j; }
-    int bi = bj >= 0 ? sub + 8 * bj : 0x7fffffff;
+    int bi = bj >= 0 ? sub + LPT * bj : 0x7fffffff;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
+    for (int o = 1; o < LPT; o <<= 1) {
       const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if ((bi & 7) == sub) taken |= 1u << (bi >> 3);
+    if (bi % LPT == sub) taken |= 1u << (bi / LPT);
     const float pr = expf(bv - m) / ssum;
     psum += pr;
     if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
   }
 }
 
-template <int NV>
+// CS: cluster size (CTAs per token tile); NV: logits per lane in the top-k.
+template <int CS, int NV>
 __global__ void __launch_bounds__(kRouterThreads, 1)
     k_router(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const RouterParams p) {
@@ -99,10 +100,12 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
-  const int cr = p.csize > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-  const int tile = blockIdx.x / p.csize;
+  constexpr int TPC = kRouterN / CS;  // tokens this CTA gates (its permutation chunk)
+  constexpr int LPT = 128 / TPC;      // lanes per token in the top-k
+  const int cr = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int tile = blockIdx.x / CS;
   const int t0 = tile * kRouterN;
-  const int kb_per = (p.H / 64) / p.csize;
+  const int kb_per = (p.H / 64) / CS;
   const int kb0 = cr * kb_per;
   const bool tr = blockIdx.x == 0;
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 0); LP_TRACE_MIN(8); }
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
 
   const int e_pad = (p.E + 31) & ~31;
   float* s_part = reinterpret_cast<float*>(smem);             // [kRouterN][e_pad] this CTA's partial logits
-  float* s_logit = s_part + kRouterN * 256;                    // [kRouterN][e_pad] full logits (leader)
+  float* s_logit = s_part + kRouterN * 256;                    // [TPC][e_pad] this CTA's token logits
   int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
   float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
   int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       }
       LP_TRACE_AT(tr, 3);
     }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, kRouterN);
@@ -163,13 +167,14 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       }
       mma_commit(tfull);
     }
+    __syncwarp();
   } else {
     // TMEM -> smem (the ring is drained once tfull fires: every MMA has read its stage)
     const int q = warp & 3;
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (threadIdx.x == 64) LP_TRACE_AT(tr, 4);
-    float* dst = p.csize > 1 ? s_part : s_logit;
+    float* dst = CS > 1 ? s_part : s_logit;
     for (int mt = 0; mt < p.mtiles; ++mt) {
       uint32_t v[16];
       tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + mt * kRouterN, v);
@@ -183,50 +188,57 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (p.csize > 1) {
+  if (threadIdx.x == 0) LP_TRACE_AT(tr, 10);
+  if (CS > 1) {
     cluster_sync();  // every CTA's partial logits are now readable over DSMEM
-    if (cr == 0 && warp >= 2) {
-      // leader: s_logit = sum_r partial_r in rank order (float4 over experts)
+    if (threadIdx.x == 0) LP_TRACE_AT(tr, 11);
+    if (warp >= 2) {
+      // this CTA's token rows: s_logit[i][e] = sum_rank partial_rank[cr*TPC + i][e] (rank order)
       const int et = threadIdx.x - 64;
-      const int nq = kRouterN * (e_pad / 4);
+      const int nq = TPC * (e_pad / 4);
       for (int idx = et; idx < nq; idx += 128) {
-        const int off = idx * 4;
-        float4 acc = *reinterpret_cast<const float4*>(s_part + off);
+        const int off = cr * TPC * e_pad + idx * 4;
         const uint32_t la = smem_u32(s_part + off);
-        for (int r = 1; r < p.csize; ++r) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
           const float4 v = ld_dsmem_f4(mapa_shared(la, r));
           acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
-        *reinterpret_cast<float4*>(s_logit + off) = acc;
+        *reinterpret_cast<float4*>(s_logit + idx * 4) = acc;
       }
     }
-    cluster_sync();  // partials consumed: non-leaders may leave
+    cluster_sync();  // partials consumed: any CTA may leave
+    if (threadIdx.x == 0) LP_TRACE_AT(tr, 12);
   }
-  if (cr == 0 && warp >= 2) {
+  if (warp >= 2) {
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
+    const int tc0 = t0 + cr * TPC;   // first token of this CTA's chunk
+    const int chunk = tile * CS + cr;
     named_bar_sync(1, 128);
-    // ---------------- softmax + top-k: 8 lanes per token ----------------
+    // ---------------- softmax + top-k: LPT lanes per token ----------------
     {
-      const int g = et >> 3;
-      const int sub = et & 7;
-      const int t = t0 + g;
+      const int g = et / LPT;
+      const int sub = et % LPT;
+      const int t = tc0 + g;
       float psum;
-      topk_8lanes<NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
-      __syncwarp();
+      topk_lanes<LPT, NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
+      named_bar_sync(1, 128);
       if (t < p.T) {
-        for (int r = sub; r < p.topk; r += 8) {
+        for (int r = sub; r < p.topk; r += LPT) {
           p.ids[static_cast<size_t>(t) * p.topk + r] = s_ids[g * 32 + r];
           p.w[static_cast<size_t>(t) * p.topk + r] = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r];
         }
       }
     }
     if (et == 0) LP_TRACE_AT(tr, 5);
-    // ---------------- stable per-tile histogram + ranks: warp q owns tokens 4q..4q+3 ----------------
+    // ---------------- stable chunk histogram + ranks: warp q owns TPC/4 tokens ----------------
+    constexpr int TPW = TPC / 4;
     for (int ee = lane; ee < e_pad; ee += 32) s_wh[q * e_pad + ee] = 0;
     __syncwarp();
-    const int tok_lo = q * 4;
-    const int n_tok = max(0, min(4, p.T - t0 - tok_lo));
+    const int tok_lo = q * TPW;
+    const int n_tok = max(0, min(TPW, p.T - tc0 - tok_lo));
     const int n_ent = n_tok * p.topk;
     const unsigned lt = (1u << lane) - 1u;
     int my_rank[4], my_e[4];
@@ -258,18 +270,19 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         s_wh[w4 * e_pad + ee] = run;
         run += c;
       }
-      if (ee < p.E) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = run;
+      if (ee < p.E) p.tile_hist[static_cast<size_t>(chunk) * p.E + ee] = run;
     }
     named_bar_sync(1, 128);
 #pragma unroll
     for (int st = 0; st < 4; ++st) {
       if (my_e[st] >= 0)
-        p.rank_local[static_cast<size_t>(t0 + tok_lo) * p.topk + st * 32 + lane] =
+        p.rank_local[static_cast<size_t>(tc0 + tok_lo) * p.topk + st * 32 + lane] =
             my_rank[st] + s_wh[q * e_pad + my_e[st]];
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 64) LP_TRACE_AT(tr, 14);
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
   if (warp == 1) {
     tc_fence_after();

@@ -23,7 +23,8 @@ NAMES = {0: "router blk0 start", 1: "router blk0 setup done", 2: "router blk0 fi
          3: "router blk0 all TMA issued", 4: "router blk0 MMA done", 5: "router blk0 top-k done",
          6: "router blk0 end", 8: "router first CTA start", 9: "router last CTA end",
          16: "scan start", 17: "scan staged", 18: "scan end (staged)",
-         24: "scatter first", 25: "scatter last", 32: "experts first CTA start", 33: "experts blk0 start",
+         24: "scatter first", 25: "scatter last", 10: "router blk0 post-mma sync", 11: "router blk0 cluster sync1",
+         12: "router blk0 cluster sync2", 13: "router blk0 top-k done(2)", 14: "router blk0 hist done", 32: "experts first CTA start", 33: "experts blk0 start",
          34: "experts last CTA end", 35: "experts blk0 end", 40: "combine first", 41: "combine last"}
 
 
@@ -54,7 +55,14 @@ def main():
             if v in (0, 2**64 - 1):
                 continue
             print(f"{NAMES[k]:32s} {(v - t0) / 1000:9.2f} us")
+        if os.environ.get("LP_ITEMS"):
+            for cta in range(4):
+                ts = [buf[64 + cta * 32 + i] for i in range(30)]
+                its = [buf[192 + cta * 32 + i] for i in range(30)]
+                row = [f"{its[i]}@{(ts[i] - t0) / 1000:.1f}" for i in range(30) if ts[i] not in (0, 2**64 - 1)]
+                print(f"cta{cta}:", " ".join(row))
 
 
 if __name__ == "__main__":
     main()
+
