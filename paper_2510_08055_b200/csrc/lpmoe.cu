@@ -79,7 +79,7 @@ struct Layout {
   size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
   size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
   int csize;         // router cluster size
-  int chunk_tokens;  // tokens per permutation chunk (= kRouterN / csize)
+  int chunk_tokens;  // tokens per permutation chunk (= router tile)
   int nchunks;
 };
 
@@ -94,7 +94,7 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
   Layout L{};
   const size_t S = static_cast<size_t>(T) * topk;
   L.csize = router_cluster((T + lp::kRouterN - 1) / lp::kRouterN, H);
-  L.chunk_tokens = lp::kRouterN / L.csize;
+  L.chunk_tokens = lp::kRouterN;
   L.nchunks = (T + L.chunk_tokens - 1) / L.chunk_tokens;
   size_t o = kHeaderBytes;
   auto take = [&](size_t bytes) {

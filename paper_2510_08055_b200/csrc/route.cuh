@@ -17,16 +17,17 @@
 // those rows of every CTA's partials over DSMEM in fixed rank order
 // (deterministic, no global round trip) and its 4 epilogue warps run
 //   * softmax + top-k with 8*csize lanes per token (all tokens concurrently);
-//   * the stable expert histogram of its token chunk + in-chunk ranks of the
-//     routing entries (match_any within a warp, exclusive scan across the 4
-//     warps), which the permutation (permute.cuh) turns into slots.
+//   * the stable expert histogram of its tokens + ranks of the routing
+//     entries (match_any within a warp, exclusive scans across the 4 warps and
+//     across the cluster's CTAs over DSMEM), so each 16-token tile gets one
+//     histogram that the permutation (permute.cuh) turns into slots.
 #pragma once
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 
 namespace lp {
 
-constexpr int kRouterN = 16;         // tokens per router tile; a chunk is kRouterN / csize tokens
+constexpr int kRouterN = 16;         // tokens per router tile (= permutation chunk)
 constexpr int kRouterStages = 6;
 constexpr int kRouterThreads = 192;  // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
 constexpr int kRouterBBytes = kRouterN * 128;
@@ -39,8 +40,8 @@ struct RouterParams {
   int mtiles;           // ceil(E / 128)
   int32_t* ids;         // [T, topk]
   float* w;             // [T, topk]
-  int32_t* tile_hist;   // [nchunks, E] per-chunk expert counts (chunk = kRouterN/CS tokens)
-  int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its chunk
+  int32_t* tile_hist;   // [ntiles, E] per-tile expert counts (tile = kRouterN tokens)
+  int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its tile
 };
 
 // Softmax + top-k of one token held by LPT consecutive lanes (lane `sub` owns
@@ -65,6 +66,27 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
   for (int o = 1; o < LPT; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
   uint32_t taken = 0;
   psum = 0.f;
+  if constexpr (LPT == 32) {
+    // whole warp per token: two redux.sync per selection round (max key, then min index)
+    for (int r = 0; r < topk; ++r) {
+      float bv = -INFINITY;
+      int bj = -1;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (!((taken >> j) & 1u) && l[j] > bv) { bv = l[j]; bj = j; }
+      const uint32_t bits = __float_as_uint(bv);
+      const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);  // order-preserving
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, bj >= 0 ? key : 0u);
+      const uint32_t cand = (bj >= 0 && key == kmax) ? static_cast<uint32_t>(sub + 32 * bj) : 0xffffffffu;
+      const int bi = static_cast<int>(__reduce_min_sync(0xffffffffu, cand));
+      if ((bi & 31) == sub) taken |= 1u << (bi >> 5);
+      const uint32_t vb = (kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax;
+      const float pr = expf(__uint_as_float(vb) - m) / ssum;
+      psum += pr;
+      if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
+    }
+    return;
+  }
   for (int r = 0; r < topk; ++r) {
     float bv = -INFINITY;
     int bj = -1;
@@ -132,6 +154,10 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
   float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
   int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
+  int32_t* s_cta = s_wh + 4 * 256;                                        // [e_pad] this CTA's chunk totals
+  int32_t* s_base = s_cta + 256;                                          // [e_pad] totals of lower ranks
+  int32_t* s_rank = s_base + 256;                                         // [128][4] in-warp ranks
+  int32_t* s_ent = s_rank + 512;                                          // [128][4] entry experts
 
   if (warp == 0) {
     if (lane == 0) {
@@ -215,7 +241,6 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
     const int tc0 = t0 + cr * TPC;   // first token of this CTA's chunk
-    const int chunk = tile * CS + cr;
     named_bar_sync(1, 128);
     // ---------------- softmax + top-k: LPT lanes per token ----------------
     {
@@ -262,7 +287,8 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       }
     }
     named_bar_sync(1, 128);
-    for (int ee = et; ee < e_pad; ee += 128) {  // exclusive scan over the 4 warps per expert
+    // exclusive scan over this CTA's 4 warps; the CTA's total goes to s_cta[e]
+    for (int ee = et; ee < e_pad; ee += 128) {
       int run = 0;
 #pragma unroll
       for (int w4 = 0; w4 < 4; ++w4) {
@@ -270,15 +296,56 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         s_wh[w4 * e_pad + ee] = run;
         run += c;
       }
-      if (ee < p.E) p.tile_hist[static_cast<size_t>(chunk) * p.E + ee] = run;
+      s_cta[ee] = run;
     }
     named_bar_sync(1, 128);
-#pragma unroll
-    for (int st = 0; st < 4; ++st) {
-      if (my_e[st] >= 0)
-        p.rank_local[static_cast<size_t>(tc0 + tok_lo) * p.topk + st * 32 + lane] =
-            my_rank[st] + s_wh[q * e_pad + my_e[st]];
+    if constexpr (CS == 1) {
+      for (int ee = et; ee < p.E; ee += 128) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = s_cta[ee];
     }
+    // (CS > 1: cross-CTA bases are applied after the cluster barrier below)
+    if constexpr (CS == 1) {
+#pragma unroll
+      for (int st = 0; st < 4; ++st) {
+        if (my_e[st] >= 0)
+          p.rank_local[static_cast<size_t>(tc0 + tok_lo) * p.topk + st * 32 + lane] =
+              my_rank[st] + s_wh[q * e_pad + my_e[st]];
+      }
+    }
+    for (int st = 0; st < 4; ++st) { s_rank[et * 4 + st] = my_rank[st]; s_ent[et * 4 + st] = my_e[st]; }
+  }
+  if constexpr (CS > 1) {
+    // tile histogram across the cluster: CTA r adds the totals of ranks < r to
+    // its ranks; the last CTA writes the tile total. Fixed order -> stable slots.
+    __syncthreads();
+    cluster_sync();
+    if (warp >= 2) {
+      const int q = warp & 3;
+      const int et = threadIdx.x - 64;
+      const int tc0 = t0 + cr * TPC;
+      constexpr int TPW = TPC / 4;
+      for (int ee = et; ee < e_pad; ee += 128) {
+        int before = 0, total = 0;
+        const uint32_t la = smem_u32(s_cta + ee);
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+          uint32_t v;
+          asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa_shared(la, r)) : "memory");
+          if (r < cr) before += static_cast<int>(v);
+          total += static_cast<int>(v);
+        }
+        s_base[ee] = before;
+        if (cr == CS - 1 && ee < p.E) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = total;
+      }
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int st = 0; st < 4; ++st) {
+        const int ex = s_ent[et * 4 + st];
+        if (ex >= 0)
+          p.rank_local[static_cast<size_t>(tc0 + q * TPW) * p.topk + st * 32 + lane] =
+              s_rank[et * 4 + st] + s_wh[q * e_pad + ex] + s_base[ex];
+      }
+    }
+    cluster_sync();  // s_cta of every CTA consumed
   }
   tc_fence_before();
   __syncthreads();
