@@ -340,7 +340,9 @@ def run_ours(args, rank: int, world: int):
                          f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                 "d2h_bytes_per_step": T * s.hidden * 2},
-        "gpu_launches": 7 * K,
+        # ours per step: fused path = router, scan, scatter, experts, combine; EP adds the
+        # standalone permutes (3 each), the expert-plan kernel and a second combine
+        "gpu_launches": (5 if world == 1 else 11) * K,
         "clocks": clocks.summary(t_region0, t_region1),
     }
     if stage_us is not None:

@@ -1,0 +1,197 @@
+"""Expert-parallel MoE layer: experts sharded over ranks,
+tokens data-parallel, one exchange step each way over NCCL.
+
+Rank r owns experts [r*E/P, (r+1)*E/P); the router weight is replicated.
+Per layer call on each rank (T_local tokens):
+
+  1. route + permute locally over the GLOBAL expert set       (K1, K2)
+     -> x_perm is expert-contiguous, hence destination-rank-contiguous
+  2. all_to_all_single of the per-(dest rank, local expert) counts
+  3. all_to_all_single of x_perm rows (uneven splits)          dispatch
+  4. permute the received rows by local expert (K2, topk=1) and run the
+     local expert FFN (K3) on the owned weights
+  5. un-permute to receive order (K4 with weight 1: exact copy) and
+     all_to_all_single the rows back                           return
+  6. weighted combine with the local routing weights           (K4)
+
+The reference has no multi-GPU code; this is the B200-native EP
+the north star asks for. All compute is liblpmoe.so through `GpuOps`; the
+exchange logic is written against a small ops protocol so it is tested with
+world-size-2 gloo on CPU (tests/test_ep.py injects CPU ops there).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .moe import MoEStats, _check_tensor, _stream_ptr
+from .types import MoEShape, require
+
+
+class GpuOps:
+    """The four C-ABI stages with explicit (E, k) so they serve both the global
+    routing (E experts, top-k) and the local re-permutation (E/P experts, k=1)."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.lib = _native.load()
+        self._ws: torch.Tensor | None = None
+
+    def _workspace(self, T: int, H: int, I: int, E: int, k: int) -> torch.Tensor:
+        need = max(int(self.lib.lp_moe_workspace_bytes(max(T, 1), H, I, E, k)), 256)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def route(self, x, wr, top_k: int, renorm: bool):
+        T, H = x.shape
+        E = wr.shape[0]
+        ids = torch.empty((T, top_k), dtype=torch.int32, device=self.device)
+        w = torch.empty((T, top_k), dtype=torch.float32, device=self.device)
+        if T:
+            ws = self._workspace(T, H, 128, E, top_k)
+            _native.check(self.lib.lp_moe_route(x.data_ptr(), wr.data_ptr(), T, H, E, top_k, int(renorm),
+                                                ids.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                _stream_ptr(self.device)), "lp_moe_route")
+        return ids, w
+
+    def permute(self, ids, x, num_experts: int):
+        T, k = ids.shape
+        H = x.shape[1]
+        S = T * k
+        counts = torch.zeros((num_experts,), dtype=torch.int32, device=self.device)
+        offsets = torch.zeros((num_experts + 1,), dtype=torch.int32, device=self.device)
+        slot_of = torch.empty((S,), dtype=torch.int32, device=self.device)
+        tok_of = torch.empty((S,), dtype=torch.int32, device=self.device)
+        x_perm = torch.empty((S, H), dtype=x.dtype, device=self.device)
+        if T:
+            ws = self._workspace(T, H, 128, num_experts, k)
+            _native.check(self.lib.lp_moe_permute(ids.data_ptr(), x.data_ptr(), T, H, num_experts, k,
+                                                  counts.data_ptr(), offsets.data_ptr(), slot_of.data_ptr(),
+                                                  tok_of.data_ptr(), x_perm.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                  _stream_ptr(self.device)), "lp_moe_permute")
+        return counts, offsets, slot_of, tok_of, x_perm
+
+    def experts(self, x_perm, offsets, w13, w2):
+        S, H = x_perm.shape
+        E, I2, _ = w13.shape
+        y_perm = torch.empty((S, H), dtype=x_perm.dtype, device=self.device)
+        if S:
+            act = torch.empty((S, I2 // 2), dtype=x_perm.dtype, device=self.device)
+            ws = self._workspace(S, H, I2 // 2, E, 1)
+            _native.check(self.lib.lp_moe_experts(x_perm.data_ptr(), offsets.data_ptr(), S, w13.data_ptr(),
+                                                  w2.data_ptr(), H, I2 // 2, E, act.data_ptr(), y_perm.data_ptr(),
+                                                  ws.data_ptr(), ws.numel(), _stream_ptr(self.device)),
+                          "lp_moe_experts")
+        return y_perm
+
+    def combine(self, y_perm, slot_of, w):
+        T, k = w.shape
+        H = y_perm.shape[1]
+        y = torch.empty((T, H), dtype=y_perm.dtype, device=self.device)
+        if T:
+            _native.check(self.lib.lp_moe_combine(y_perm.data_ptr(), slot_of.data_ptr(), w.data_ptr(), T, H, k,
+                                                  y.data_ptr(), _stream_ptr(self.device)), "lp_moe_combine")
+        return y
+
+
+@dataclass
+class EPStats:
+    counts: torch.Tensor       # int32 [E] global-expert counts of this rank's tokens
+    recv_rows: int             # rows this rank's experts processed
+    send_splits: list[int]
+    recv_splits: list[int]
+    shape: MoEShape
+
+    @property
+    def local(self) -> MoEStats:
+        return MoEStats(self.counts, self.shape)
+
+
+class EPMoE:
+    """One MoE layer, experts sharded over the ranks of `group`."""
+
+    def __init__(self, shape: MoEShape, wr: torch.Tensor, w13_local: torch.Tensor, w2_local: torch.Tensor,
+                 rank: int, world: int, group=None, ops=None):
+        E = shape.num_experts
+        require(E % world == 0, f"num_experts={E} must be divisible by the EP world size {world}")
+        self.shape, self.rank, self.world, self.group = shape, rank, world, group
+        self.e_local = E // world
+        self.e0 = rank * self.e_local
+        H, I = shape.hidden, shape.ffn
+        require(tuple(wr.shape) == (E, H), f"wr must have shape {(E, H)}, got {tuple(wr.shape)}")
+        require(tuple(w13_local.shape) == (self.e_local, 2 * I, H),
+                f"w13_local must have shape {(self.e_local, 2 * I, H)}, got {tuple(w13_local.shape)}")
+        require(tuple(w2_local.shape) == (self.e_local, H, I),
+                f"w2_local must have shape {(self.e_local, H, I)}, got {tuple(w2_local.shape)}")
+        self.wr, self.w13, self.w2 = wr, w13_local, w2_local
+        self.device = wr.device
+        if ops is None:
+            for name, t in (("wr", wr), ("w13_local", w13_local), ("w2_local", w2_local)):
+                _check_tensor(name, t, tuple(t.shape), torch.bfloat16)
+            ops = GpuOps(self.device)
+        self.ops = ops
+        self._ones: dict[int, torch.Tensor] = {}
+
+    @classmethod
+    def from_full(cls, shape: MoEShape, wr, w13, w2, rank: int, world: int, group=None, ops=None) -> "EPMoE":
+        el = shape.num_experts // world
+        sl = slice(rank * el, (rank + 1) * el)
+        return cls(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, group, ops)
+
+    def _ones_w(self, n: int) -> torch.Tensor:
+        t = self._ones.get(n)
+        if t is None:
+            t = torch.ones((n, 1), dtype=torch.float32, device=self.device)
+            self._ones[n] = t
+        return t
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, EPStats]:
+        s, P, el = self.shape, self.world, self.e_local
+        require(x.dim() == 2 and x.shape[1] == s.hidden, f"x must be [T, {s.hidden}], got {tuple(x.shape)}")
+        ids, w = self.ops.route(x, self.wr, s.top_k, s.norm_topk_prob)
+        counts, offsets, slot_of, tok_of, x_perm = self.ops.permute(ids, x, s.num_experts)
+        # (2) counts per (destination rank, its local expert)
+        send_counts = counts.view(P, el).contiguous()
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        both = torch.stack([send_counts.sum(1), recv_counts.sum(1)]).cpu()  # one host sync per layer
+        send_splits, recv_splits = both[0].tolist(), both[1].tolist()
+        R = int(sum(recv_splits))
+        # (3) dispatch: x_perm is destination-contiguous because slots are expert-contiguous
+        x_recv = torch.empty((R, s.hidden), dtype=x.dtype, device=self.device)
+        dist.all_to_all_single(x_recv, x_perm, recv_splits, send_splits, group=self.group)
+        # (4) group received rows by local expert (stable: source rank, then source order) and run them
+        local_ids = torch.repeat_interleave(
+            torch.arange(el, device=self.device, dtype=torch.int32).repeat(P),
+            recv_counts.reshape(-1).to(torch.int64), output_size=R).view(R, 1)
+        _, off_l, slot_l, _, x_loc = self.ops.permute(local_ids, x_recv, el)
+        y_loc = self.ops.experts(x_loc, off_l, self.w13, self.w2)
+        # (5) back to receive order (weight 1.0: exact) and return to the source ranks
+        y_recv = self.ops.combine(y_loc, slot_l, self._ones_w(R))
+        y_back = torch.empty((x_perm.shape[0], s.hidden), dtype=x.dtype, device=self.device)
+        dist.all_to_all_single(y_back, y_recv, send_splits, recv_splits, group=self.group)
+        # (6) weighted combine of this rank's tokens
+        y = self.ops.combine(y_back, slot_of, w)
+        if out is not None:
+            out.copy_(y)
+            y = out
+        self.last_ids, self.last_weights = ids, w
+        return y, EPStats(counts, R, send_splits, recv_splits, s)
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None,
+                     x_dev: torch.Tensor | None = None):
+        """End-to-end call with host buffers: H2D copy, EP layer, D2H copy."""
+        xd = x_dev if x_dev is not None else torch.empty(x_host.shape, dtype=x_host.dtype, device=self.device)
+        xd.copy_(x_host, non_blocking=True)
+        yd, stats = self.forward(xd)
+        if y_host is None:
+            y_host = torch.empty(yd.shape, dtype=yd.dtype, pin_memory=True)
+        y_host.copy_(yd, non_blocking=True)
+        return y_host, stats
