@@ -1,0 +1,152 @@
+"""Layered executor: drives real MoE layers on the B200 from the serving planner.
+
+SURVEY.md §8(f) row 1. `MeasuredCost` plugs into `serving.run` in place of the
+modelled roofline: for every planned iteration (a `BatchPlan`) it runs the
+iteration's MoE work through a stack of resident `GpuMoE` layers and charges
+the measured device time; attention / dense projections stay modelled
+(out of scope) with the reference formulas on B200 peaks.
+
+Per iteration and per MoE layer l the routed batch is exactly what the
+reference engine charges at engine.py:137-154: every decoding request's token
+plus the prefill slices whose layer range contains l. Hidden states:
+  * each prefilling request owns a stash [input_len, H] (bf16) that carries its
+    prompt activations between iterations (layered: after group g; chunked:
+    the processed chunk rows);
+  * each decoding request owns one row, carried from iteration to iteration;
+  * layers are applied as a residual stream h <- h + MoE_l(h), so routing sees
+    O(1) activations at every depth (the MoE-only model has no attention/norm).
+Layers whose active row set is identical are run back to back on one
+contiguous buffer (decode rows first, then the slices), so a layered
+iteration is two buffers (designated group: decode+prompt rows, other layers:
+decode rows) and a chunked iteration is one.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import costmodel as cm
+from .moe import GpuMoE
+from .serving import BatchPlan, ServingState, attention_kernels
+from .synthetic import router_weight
+from .types import ModelSpec, MoEShape
+
+
+class MoEModel:
+    """`num_layers` resident MoE layers of `shape` with random-init weights."""
+
+    def __init__(self, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0, std: float = 0.02):
+        self.shape, self.num_layers = shape, num_layers
+        self.device = torch.device(device)
+        self.layers: list[GpuMoE] = []
+        for i in range(num_layers):
+            g = torch.Generator(device=self.device).manual_seed(seed * 1000 + i)
+            E, H, I = shape.num_experts, shape.hidden, shape.ffn
+            w13 = (torch.randn((E, 2 * I, H), generator=g, device=self.device) * std).to(torch.bfloat16)
+            w2 = (torch.randn((E, H, I), generator=g, device=self.device) * std).to(torch.bfloat16)
+            wr = router_weight(E, H, seed * 1000 + i).to(self.device)
+            self.layers.append(GpuMoE(shape, wr, w13, w2))
+
+    def run_segment(self, x: torch.Tensor, l0: int, l1: int, hits: torch.Tensor) -> torch.Tensor:
+        """h <- h + MoE_l(h) for l in [l0, l1); accumulates experts hit per layer into hits (device)."""
+        for layer in range(l0, l1):
+            y, stats = self.layers[layer](x)
+            x.add_(y)
+            hits[layer] += (stats.counts > 0).sum()
+        return x
+
+
+class MeasuredCost:
+    """serving.run cost plug-in: measured MoE device time + modelled attention/dense."""
+
+    def __init__(self, model_spec: ModelSpec, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False):
+        assert stack.num_layers == model_spec.num_layers
+        self.spec, self.stack = model_spec, stack
+        self.keep_final_prompt = keep_final_prompt
+        self.final_prompt: dict[int, torch.Tensor] = {}
+        self.dev = stack.device
+        self.H = stack.shape.hidden
+        self.stash: dict[int, torch.Tensor] = {}    # rid -> [input_len, H] prompt activations
+        self.decode_row: dict[int, torch.Tensor] = {}  # rid -> [H] current decode hidden
+        self.embed_seed = embed_seed
+        self.iter_log: list[dict] = []
+
+    def _prompt(self, st: ServingState, rid: int) -> torch.Tensor:
+        h = self.stash.get(rid)
+        if h is None:
+            r = st.by_id[rid]
+            g = torch.Generator(device=self.dev).manual_seed(self.embed_seed * 1_000_003 + rid)
+            h = torch.randn((r.input_len, self.H), generator=g, device=self.dev).to(torch.bfloat16)
+            self.stash[rid] = h
+        return h
+
+    def _decode_rows(self, st: ServingState, plan: BatchPlan) -> list[torch.Tensor]:
+        rows = []
+        for rid in plan.decode_ids:
+            row = self.decode_row.get(rid)
+            if row is None:  # prefill finished last iteration: its last prompt row seeds decoding
+                h = self.stash.pop(rid)
+                if self.keep_final_prompt:
+                    self.final_prompt[rid] = h
+                row = h[-1].clone()
+                self.decode_row[rid] = row
+            rows.append(row)
+        return rows
+
+    def iteration(self, st: ServingState, plan: BatchPlan, decode_ctx: int) -> list[cm.Kernel]:
+        L = self.spec.num_layers
+        for rid in [k for k in self.stash if st.by_id[k].phase == "finished"]:
+            h = self.stash.pop(rid)  # prompt finished without a decode step (output_len == 1)
+            if self.keep_final_prompt:
+                self.final_prompt[rid] = h
+        dec_rows = self._decode_rows(st, plan)
+        D = len(dec_rows)
+        cuts = sorted({0, L} | {a.layer_start for a in plan.prefill_assignments}
+                      | {a.layer_end for a in plan.prefill_assignments})
+        hits = torch.zeros(L, dtype=torch.int64, device=self.dev)
+        routed = plan.layer_token_counts(L)
+        stream = torch.cuda.current_stream(self.dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dec = torch.stack(dec_rows) if D else torch.empty((0, self.H), dtype=torch.bfloat16, device=self.dev)
+        for l0, l1 in zip(cuts, cuts[1:]):
+            act = [a for a in plan.prefill_assignments if a.layer_start <= l0 < a.layer_end]
+            parts = [dec] + [self._prompt(st, a.request_id)[a.token_start:a.token_end] for a in act]
+            if sum(p.shape[0] for p in parts) == 0:
+                continue
+            x = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
+            x = self.stack.run_segment(x, l0, l1, hits)
+            dec = x[:D]
+            off = D
+            for a in act:
+                n = a.num_tokens
+                self._prompt(st, a.request_id)[a.token_start:a.token_end].copy_(x[off:off + n])
+                off += n
+        e1.record(stream)
+        for rid, row in zip(plan.decode_ids, dec):
+            self.decode_row[rid] = row
+        torch.cuda.synchronize(self.dev)
+        moe_s = e0.elapsed_time(e1) * 1e-3
+        nnz = hits.cpu().tolist()
+        expert_bytes = float(sum(nnz) * self.spec.bytes_per_expert)
+        act_bytes = float(sum(2 * n * self.spec.hidden_dim * self.spec.dtype_bytes for n in routed))
+        flops = float(sum(n * self.spec.top_k * self.spec.flops_per_token_per_expert for n in routed))
+        ks = [cm.Kernel(cm.MOE, flops, expert_bytes + act_bytes, expert_bytes, measured_s=moe_s)]
+        # modelled non-MoE work (same formulas as the reference engine), on B200 peaks
+        scopes: dict[tuple[int, int], int] = {}
+        for a in plan.prefill_assignments:
+            scopes[(a.layer_start, a.layer_end)] = scopes.get((a.layer_start, a.layer_end), 0) + a.num_tokens
+        covered = 0
+        for (ls, le), pf in sorted(scopes.items()):
+            covered += le - ls
+            ks.append(cm.dense_cost(self.spec, D + pf, le - ls))
+        if L - covered > 0 and D > 0:
+            ks.append(cm.dense_cost(self.spec, D, L - covered))
+        ks.extend(attention_kernels(self.spec, plan, decode_ctx))
+        self.iter_log.append({"moe_s": moe_s, "routed": routed, "experts_hit": nnz, "decode": D,
+                              "prefill_tokens": plan.prefill_tokens})
+        # drop finished requests' state
+        live = {r.id for r in st.decoding} | set(plan.decode_ids)
+        for rid in [k for k in self.decode_row if k not in live]:
+            del self.decode_row[rid]
+        return ks
