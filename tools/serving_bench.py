@@ -22,7 +22,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2510_08055_b200 import QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL  # noqa: E402
+from paper_2510_08055_b200.types import QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL  # noqa: E402
 from paper_2510_08055_b200 import costmodel as cm  # noqa: E402
 from paper_2510_08055_b200 import serving as sv  # noqa: E402
 
