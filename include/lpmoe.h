@@ -99,6 +99,14 @@ int lp_union_counts_uniform(const double* u, int trials, int batch, int k, int E
 int lp_union_counts_weighted(const double* u, int trials, int batch, int k, int E, const double* weights,
                              int64_t* out, void* stream);
 
+/* Executor glue between layers (serving.py / executor.py, not the MoE hot
+ * path): h += delta (if delta != NULL, in place, bf16), then
+ * xn = h * rsqrt(mean(h^2) + eps) per row — the residual update and the
+ * pre-MoE RMSNorm of a Qwen3 decoder layer with unit gain. Stands in for the
+ * non-MoE layer work the reference charges via dense_cost
+ * (costmodel.py:128-145, engine.py:149). h, delta, xn [T,H] bf16. */
+int lp_add_rmsnorm(void* h, const void* delta, void* xn, int T, int H, float eps, void* stream);
+
 /* Profiling hook (calling thread only): when n >= 5, the next lp_moe_forward
  * calls record events[0..4] (cudaEvent_t handles) on their stream at the
  * stage boundaries route | permute | experts | combine | end. n = 0 clears. */

@@ -38,6 +38,7 @@ SIGNATURES = {
     "lp_moe_forward": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _sz, _p]),
     "lp_union_counts_uniform": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "lp_union_counts_weighted": (_i, [_p, _i, _i, _i, _i, _p, _p, _p]),
+    "lp_add_rmsnorm": (_i, [_p, _p, _p, _i, _i, ctypes.c_float, _p]),
     "lp_profile_events": (_i, [_p, _i]),
 }
 

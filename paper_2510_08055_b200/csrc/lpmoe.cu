@@ -15,6 +15,7 @@
 
 #include "../../include/lpmoe.h"
 #include "experts_sm100.cuh"
+#include "norm.cuh"
 #include "permute.cuh"
 #include "route.cuh"
 #include "union_counts.cuh"
@@ -520,6 +521,19 @@ int lp_union_counts_weighted(const double* u, int trials, int batch, int k, int 
   const size_t sm = E * sizeof(double) + ((E + 31) / 32) * sizeof(uint32_t);
   lp::k_union_weighted<<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, weights, out);
   LP_CHECK_LAUNCH("k_union_weighted");
+  return ok();
+}
+
+int lp_add_rmsnorm(void* h, const void* delta, void* xn, int T, int H, float eps, void* stream) {
+  if (T < 0 || H <= 0 || H % 8) return fail(LP_EINVAL, "lp_add_rmsnorm: bad shape T=%d H=%d", T, H);
+  if (!(eps >= 0.f)) return fail(LP_EINVAL, "lp_add_rmsnorm: eps must be >= 0");
+  if (T == 0) return ok();
+  if (!h || !xn) return fail(LP_EINVAL, "lp_add_rmsnorm: null pointer argument");
+  if (!aligned16(h) || !aligned16(xn) || (delta && !aligned16(delta)))
+    return fail(LP_EINVAL, "lp_add_rmsnorm: tensors must be 16-byte aligned");
+  LP_CUDA(launch_pdl(lp::k_add_rmsnorm, (T + lp::kNormWarps - 1) / lp::kNormWarps, 32 * lp::kNormWarps, 0,
+                     static_cast<cudaStream_t>(stream), static_cast<__nv_bfloat16*>(h),
+                     static_cast<const __nv_bfloat16*>(delta), static_cast<__nv_bfloat16*>(xn), T, H, eps));
   return ok();
 }
 

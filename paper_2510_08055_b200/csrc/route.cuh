@@ -31,6 +31,7 @@ constexpr int kRouterN = 16;         // tokens per router tile (= permutation ch
 constexpr int kRouterStages = 6;
 constexpr int kRouterThreads = 192;  // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
 constexpr int kRouterBBytes = kRouterN * 128;
+constexpr int kRouterTmemCols = 128;  // 4 partial sums x 2 m-tiles x 16 tokens
 __host__ __device__ constexpr int router_smem_bytes(int mtiles) {
   return 1024 + kRouterStages * (mtiles * 16384 + kRouterBBytes) + 256;
 }
@@ -55,6 +56,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
   for (int j = 0; j < NV; ++j) {
     const int ex = sub + LPT * j;
     l[j] = (ex < E) ? row[ex] : -INFINITY;
+    if (l[j] != l[j]) l[j] = -INFINITY;  // NaN logits rank last (ids stay in range)
     m = fmaxf(m, l[j]);
   }
 #pragma unroll
@@ -73,7 +75,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
       int bj = -1;
 #pragma unroll
       for (int j = 0; j < NV; ++j)
-        if (!((taken >> j) & 1u) && l[j] > bv) { bv = l[j]; bj = j; }
+        if (sub + 32 * j < E && !((taken >> j) & 1u) && (bj < 0 || l[j] > bv)) { bv = l[j]; bj = j; }
       const uint32_t bits = __float_as_uint(bv);
       const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);  // order-preserving
       const uint32_t kmax = __reduce_max_sync(0xffffffffu, bj >= 0 ? key : 0u);
@@ -92,13 +94,15 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
     int bj = -1;
 #pragma unroll
     for (int j = 0; j < NV; ++j)  // ascending expert index: the first maximum wins ties
-      if (!((taken >> j) & 1u) && l[j] > bv) { bv = l[j]; bj = j; }
+      if (sub + LPT * j < E && !((taken >> j) & 1u) && (bj < 0 || l[j] > bv)) { bv = l[j]; bj = j; }
     int bi = bj >= 0 ? sub + LPT * bj : 0x7fffffff;
 #pragma unroll
     for (int o = 1; o < LPT; o <<= 1) {
       const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      if (ov > bv || (ov == bv && oi < bi) || bi == 0x7fffffff) {
+        if (oi != 0x7fffffff) { bv = ov; bi = oi; }
+      }
     }
     if (bi % LPT == sub) taken |= 1u << (bi / LPT);
     const float pr = expf(bv - m) / ssum;
@@ -127,7 +131,15 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   const int cr = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int tile = blockIdx.x / CS;
   const int t0 = tile * kRouterN;
-  const int kb_per = (p.H / 64) / CS;
+  // K = H is summed as NPART fixed partial sums (each a separate TMEM
+  // accumulator, folded left in part order), whatever the cluster size: the
+  // fp32 logits of a token are then bit-identical for every batch size and
+  // batch composition (layered vs chunked prefill see the same per-token math).
+  const int kb_total = p.H / 64;
+  const int npart = (kb_total % 4 == 0) ? 4 : ((kb_total % 2 == 0) ? 2 : 1);
+  const int ppc = npart / CS;               // partial sums owned by this CTA
+  const int kb_part = kb_total / npart;     // k-blocks per partial sum
+  const int kb_per = ppc * kb_part;
   const int kb0 = cr * kb_per;
   const bool tr = blockIdx.x == 0;
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 0); LP_TRACE_MIN(8); }
@@ -139,7 +151,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     prefetch_tmap(&tm_wr);
     prefetch_tmap(&tm_x);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 32);
+  if (warp == 1) tmem_alloc(tmem_slot, kRouterTmemCols);
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
@@ -149,8 +161,8 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   if (threadIdx.x == 0) LP_TRACE_AT(tr, 1);
 
   const int e_pad = (p.E + 31) & ~31;
-  float* s_part = reinterpret_cast<float*>(smem);             // [kRouterN][e_pad] this CTA's partial logits
-  float* s_logit = s_part + kRouterN * 256;                    // [TPC][e_pad] this CTA's token logits
+  float* s_part = reinterpret_cast<float*>(smem);             // [ppc][kRouterN][e_pad] this CTA's partial logits
+  float* s_logit = s_part + 4 * kRouterN * 256;                // [TPC][e_pad] this CTA's token logits
   int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
   float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
   int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
@@ -183,11 +195,12 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * stage_bytes);
         const uint64_t b = sdesc_kmajor_sw128(sa + p.mtiles * 16384);
+        const uint32_t d0 = tmem_base + (i / kb_part) * (p.mtiles * kRouterN);
         for (int mt = 0; mt < p.mtiles; ++mt) {
           const uint64_t a = sdesc_kmajor_sw128(sa + mt * 16384);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16(tmem_base + mt * kRouterN, a + 2 * k, b + 2 * k, idesc, (i | k) != 0);
+            mma_bf16(d0 + mt * kRouterN, a + 2 * k, b + 2 * k, idesc, ((i % kb_part) | k) != 0);
         }
         mma_commit(&empty[s]);
       }
@@ -200,15 +213,26 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (threadIdx.x == 64) LP_TRACE_AT(tr, 4);
-    float* dst = CS > 1 ? s_part : s_logit;
     for (int mt = 0; mt < p.mtiles; ++mt) {
-      uint32_t v[16];
-      tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + mt * kRouterN, v);
-      tmem_wait_ld();
       const int e = mt * 128 + 32 * q + lane;
-      if (e < e_pad) {
+      float acc[kRouterN];
+      for (int pl = 0; pl < ppc; ++pl) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (pl * p.mtiles + mt) * kRouterN, v);
+        tmem_wait_ld();
+        if (CS > 1) {  // parked for the cluster-wide fold below
+          if (e < e_pad) {
 #pragma unroll
-        for (int i = 0; i < kRouterN; ++i) dst[i * e_pad + e] = __uint_as_float(v[i]);
+            for (int i = 0; i < kRouterN; ++i) s_part[(pl * kRouterN + i) * e_pad + e] = __uint_as_float(v[i]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kRouterN; ++i) acc[i] = pl ? acc[i] + __uint_as_float(v[i]) : __uint_as_float(v[i]);
+        }
+      }
+      if (CS == 1 && e < e_pad) {
+#pragma unroll
+        for (int i = 0; i < kRouterN; ++i) s_logit[i * e_pad + e] = acc[i];
       }
     }
   }
@@ -224,12 +248,17 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       const int nq = TPC * (e_pad / 4);
       for (int idx = et; idx < nq; idx += 128) {
         const int off = cr * TPC * e_pad + idx * 4;
-        const uint32_t la = smem_u32(s_part + off);
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < CS; ++r) {
-          const float4 v = ld_dsmem_f4(mapa_shared(la, r));
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+          for (int pl = 0; pl < ppc; ++pl) {  // global part order r*ppc + pl
+            const float4 v = ld_dsmem_f4(mapa_shared(smem_u32(s_part + pl * kRouterN * e_pad + off), r));
+            if (r == 0 && pl == 0) {
+              acc = v;
+            } else {
+              acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+          }
         }
         *reinterpret_cast<float4*>(s_logit + idx * 4) = acc;
       }
@@ -353,7 +382,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 32);
+    tmem_dealloc(tmem_base, kRouterTmemCols);
   }
 }
 

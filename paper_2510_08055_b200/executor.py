@@ -26,7 +26,7 @@ from __future__ import annotations
 import torch
 
 from . import costmodel as cm
-from .moe import GpuMoE
+from .moe import GpuMoE, add_rmsnorm
 from .serving import BatchPlan, ServingState, attention_kernels
 from .synthetic import router_weight
 from .types import ModelSpec, MoEShape
@@ -47,12 +47,21 @@ class MoEModel:
             wr = router_weight(E, H, seed * 1000 + i).to(self.device)
             self.layers.append(GpuMoE(shape, wr, w13, w2))
 
-    def run_segment(self, x: torch.Tensor, l0: int, l1: int, hits: torch.Tensor) -> torch.Tensor:
-        """h <- h + MoE_l(h) for l in [l0, l1); accumulates experts hit per layer into hits (device)."""
-        for layer in range(l0, l1):
-            y, stats = self.layers[layer](x)
-            x.add_(y)
-            hits[layer] += (stats.counts > 0).sum()
+    def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor) -> torch.Tensor:
+        """h <- h + MoE_l(RMSNorm(h)) for l in [l0, l1) (Qwen3's pre-MoE norm keeps the
+        residual stream bounded); per-expert counts of layer l are added into counts[l]."""
+        T = x.shape[0]
+        xn = torch.empty_like(x)
+        y = torch.empty_like(x)
+        c = torch.empty((l1 - l0, self.shape.num_experts), dtype=torch.int32, device=self.device)
+        delta = None
+        for i, layer in enumerate(range(l0, l1)):
+            add_rmsnorm(x, delta, xn)
+            self.layers[layer](xn, out=y, counts_out=c[i])
+            delta = y
+        if delta is not None and T:
+            add_rmsnorm(x, delta, xn)
+        counts[l0:l1] += c
         return x
 
 
@@ -103,7 +112,7 @@ class MeasuredCost:
         D = len(dec_rows)
         cuts = sorted({0, L} | {a.layer_start for a in plan.prefill_assignments}
                       | {a.layer_end for a in plan.prefill_assignments})
-        hits = torch.zeros(L, dtype=torch.int64, device=self.dev)
+        counts = torch.zeros((L, self.stack.shape.num_experts), dtype=torch.int32, device=self.dev)
         routed = plan.layer_token_counts(L)
         stream = torch.cuda.current_stream(self.dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -115,7 +124,7 @@ class MeasuredCost:
             if sum(p.shape[0] for p in parts) == 0:
                 continue
             x = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
-            x = self.stack.run_segment(x, l0, l1, hits)
+            x = self.stack.run_segment(x, l0, l1, counts)
             dec = x[:D]
             off = D
             for a in act:
@@ -127,7 +136,7 @@ class MeasuredCost:
             self.decode_row[rid] = row
         torch.cuda.synchronize(self.dev)
         moe_s = e0.elapsed_time(e1) * 1e-3
-        nnz = hits.cpu().tolist()
+        nnz = (counts > 0).sum(dim=1).cpu().tolist()
         expert_bytes = float(sum(nnz) * self.spec.bytes_per_expert)
         act_bytes = float(sum(2 * n * self.spec.hidden_dim * self.spec.dtype_bytes for n in routed))
         flops = float(sum(n * self.spec.top_k * self.spec.flops_per_token_per_expert for n in routed))

@@ -100,8 +100,13 @@ class GpuMoE:
         return b
 
     # ------------------------------------------------------------ full layer
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, MoEStats]:
-        """y = MoE(x). x: [T, H] bf16 CUDA. Returns (y, stats); ids/weights in stats buffers."""
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                counts_out: torch.Tensor | None = None) -> tuple[torch.Tensor, MoEStats]:
+        """y = MoE(x). x: [T, H] bf16 CUDA. Returns (y, stats); ids/weights in stats buffers.
+
+        counts_out (int32 [E], optional) receives the per-expert counts instead of
+        the layer's internal per-T buffer (the executor keeps one row per layer).
+        """
         s = self.shape
         require(x.dim() == 2, f"x must be 2-D [T, H], got {tuple(x.shape)}")
         T = x.shape[0]
@@ -109,6 +114,9 @@ class GpuMoE:
         y = torch.empty_like(x) if out is None else out
         _check_tensor("out", y, (T, s.hidden), torch.bfloat16)
         ids, w, counts = self._bufs(T)
+        if counts_out is not None:
+            _check_tensor("counts_out", counts_out, (s.num_experts,), torch.int32)
+            counts = counts_out
         ws = self.workspace(T)
         rc = self._lib.lp_moe_forward(
             x.data_ptr(), self.wr.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
@@ -206,3 +214,15 @@ def layer_from_seed(shape: MoEShape, seed: int, device: str = "cuda", tie_break:
     wr = router_weight(shape.num_experts, shape.hidden, seed, tie_break=tie_break)
     w13, w2 = expert_weights(shape.num_experts, shape.hidden, shape.ffn, seed + 1)
     return GpuMoE(shape, wr.to(device), w13.to(device), w2.to(device))
+
+
+def add_rmsnorm(h: torch.Tensor, delta: torch.Tensor | None, xn: torch.Tensor, eps: float = 1e-6) -> None:
+    """h += delta (if given); xn = RMSNorm(h) with unit gain (lp_add_rmsnorm, executor glue)."""
+    require(h.is_cuda and h.dtype == torch.bfloat16 and h.dim() == 2 and h.is_contiguous(),
+            "h must be a contiguous CUDA bf16 [T, H] tensor")
+    _check_tensor("xn", xn, tuple(h.shape), torch.bfloat16)
+    if delta is not None:
+        _check_tensor("delta", delta, tuple(h.shape), torch.bfloat16)
+    rc = _native.load().lp_add_rmsnorm(h.data_ptr(), delta.data_ptr() if delta is not None else None,
+                                       xn.data_ptr(), h.shape[0], h.shape[1], eps, _stream_ptr(h.device))
+    _native.check(rc, "lp_add_rmsnorm")

@@ -160,3 +160,39 @@ def test_rejects_cpu_tensor(cuda):
     _, _, _, layer = make(TINY, 11, cuda)
     with pytest.raises(ValidationError, match="CUDA"):
         layer(torch.zeros((4, TINY.hidden), dtype=torch.bfloat16))
+
+
+def test_router_nan_rows_stay_in_range(cuda):
+    """Non-finite activations must never produce an out-of-range expert id (no OOB scatter)."""
+    s = QWEN3_30B_A3B
+    _, _, _, layer = make(s, 0, cuda)
+    x = router_tokens(64, s.hidden, 5)
+    x[3] = float("nan")
+    x[7, :100] = float("inf")
+    x[9] = 0.0
+    y, stats = layer(x.to(cuda))
+    torch.cuda.synchronize()
+    ids = layer.last_ids.cpu()
+    assert int(ids.min()) >= 0 and int(ids.max()) < s.num_experts
+    for t in range(64):  # every token still picks k distinct experts
+        assert len(set(ids[t].tolist())) == s.top_k
+    assert int(stats.counts.sum()) == 64 * s.top_k
+
+
+@pytest.mark.parametrize("T,with_delta", [(1, False), (37, True), (4100, True)])
+def test_add_rmsnorm_matches_torch(cuda, T, with_delta):
+    from paper_2510_08055_b200.moe import add_rmsnorm
+
+    g = torch.Generator().manual_seed(T)
+    h = (torch.randn((T, 2048), generator=g) * 3).to(torch.bfloat16)
+    d = (torch.randn((T, 2048), generator=g)).to(torch.bfloat16) if with_delta else None
+    hd = h.to(cuda)
+    xn = torch.empty_like(hd)
+    add_rmsnorm(hd, d.to(cuda) if d is not None else None, xn, 1e-6)
+    torch.cuda.synchronize()
+    ref_h = (h.float() + d.float()).to(torch.bfloat16) if d is not None else h
+    assert torch.equal(hd.cpu(), ref_h)
+    hf = ref_h.float()
+    ref = hf * torch.rsqrt(hf.pow(2).mean(dim=1, keepdim=True) + 1e-6)
+    err = (xn.cpu().float() - ref).norm() / ref.norm()
+    assert err < 4e-3, err
