@@ -23,15 +23,18 @@
 // precede all DN items, so a DN wait can only target items already claimed
 // by running CTAs (deadlock-free without co-residency guarantees).
 //
-// Warp roles (256 threads): w0 TMA producer + scheduler, w1 MMA issuer,
-// w2 TMEM allocator, w4..w7 epilogue (TMEM lanes 32*(w%4) ...).
+// Warp roles (384 threads): w0 TMA producer + scheduler, w1 MMA issuer,
+// w2 TMEM allocator, w4..w11 epilogue: warp w drains TMEM lanes 32*(w%4) ...,
+// warps 4..7 the even 16-column chunks and 8..11 the odd ones, so the
+// accumulator is released twice as fast (it is single-buffered at N=256).
 #pragma once
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 
 namespace lp {
 
-constexpr int kExpertsThreads = 256;
+constexpr int kExpertsThreads = 384;  // w0 TMA+sched, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
+constexpr int kEpiThreads = 256;
 constexpr int kTileM = 128;        // weight rows per tile
 constexpr int kTileK = 64;         // bf16 elements per 128-byte swizzle row
 constexpr int kBoxRows = 32;       // token rows per B-operand TMA box
@@ -49,7 +52,90 @@ struct ExpertsParams {
   __nv_bfloat16* y_perm;       // [S, H]
   uint32_t* sched;             // [0] work counter, [1+e] UP items done for expert e
   int prefetch_kblocks;        // k-blocks of the first item's W13 rows to warm in L2 before pdl_wait
+  int lookahead;               // L2 prefetch distance (k-blocks) for weight tiles ahead of the smem ring; 0 = off
+  int weights_evict_first;     // weights loaded with L2::evict_first (1) or evict_normal (0)
+  // Fused combine (y != nullptr): DN items count, per (token, 256-feature
+  // block), how many of the token's topk slots are final; the item that
+  // completes a block sums the token's topk y_perm rows in fixed j order
+  // (bit-identical to k_combine) and writes y. Counters are zero on entry and
+  // left zero (the completing item resets them).
+  __nv_bfloat16* y;            // [T, H] or nullptr (separate k_combine)
+  const int32_t* slot_tok;     // [S] token of each slot
+  const int32_t* slot_of;      // [T*topk] slot of each routing entry
+  const float* wgt;            // [T*topk] routing weights
+  uint32_t* blk_cnt;           // [T * ceil(H/256)] completion counters
+  int topk;
 };
+
+// DN-item tail of the fused combine (256 epilogue threads, named barrier 1).
+// Release: every thread's y_perm stores precede the barrier, and each thread's
+// acq_rel counter increment is cumulative over them; acquire: the completing
+// increment, then the barrier, then L2 (ld.cg) reads of the other items' rows.
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fused_combine(const ExpertsParams& p, int m0, int row0, int nvalid, int et,
+                                              int32_t* s_fin) {
+  const int nfb = (p.H + 255) / 256;
+  const int fb = m0 / 256;
+  if (et == 0) s_fin[kEpiThreads] = 0;
+  named_bar_sync(1, kEpiThreads);
+  if (et < nvalid) {
+    const int t = __ldcg(p.slot_tok + row0 + et);
+    uint32_t* c = p.blk_cnt + static_cast<size_t>(t) * nfb + fb;
+    if (atom_add_acqrel_gpu(c, 1u) == static_cast<uint32_t>(p.topk - 1)) {
+      *c = 0u;  // every increment of this call has happened: reset for the next call
+      s_fin[atomicAdd(&s_fin[kEpiThreads], 1)] = t;
+    }
+  }
+  named_bar_sync(1, kEpiThreads);
+  const int nfin = s_fin[kEpiThreads];
+  const int width = min(256, p.H - m0);  // features in this block (multiple of 128)
+  const int lane = et & 31;
+  for (int i = et >> 5; i < nfin; i += kEpiThreads / 32) {
+    const int t = s_fin[i];
+    if (lane * 8 < width) {
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      for (int j0 = 0; j0 < p.topk; j0 += 8) {  // fixed j order: bit-identical to k_combine
+        // all index / weight loads, then all row loads in flight, then the ordered sum
+        int slot[8];
+        float wj[8];
+        uint4 d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = j0 + u < p.topk;
+          slot[u] = ok ? __ldcg(p.slot_of + static_cast<size_t>(t) * p.topk + j0 + u) : 0;
+          wj[u] = ok ? __ldcg(p.wgt + static_cast<size_t>(t) * p.topk + j0 + u) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u < p.topk)
+            d[u] = __ldcg(reinterpret_cast<const uint4*>(p.y_perm + static_cast<size_t>(slot[u]) * p.H + m0) + lane);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (j0 + u < p.topk) {
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d[u]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(h2[q]);
+              acc[2 * q] += wj[u] * f.x;
+              acc[2 * q + 1] += wj[u] * f.y;
+            }
+          }
+        }
+      }
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o2[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+      reinterpret_cast<uint4*>(p.y + static_cast<size_t>(t) * p.H + m0)[lane] = o;
+    }
+  }
+}
 
 template <int MAX_N>
 struct ExpertsCfg {
@@ -61,13 +147,23 @@ struct ExpertsCfg {
   static constexpr int kTmemCols = kAccStages * kAccCols < 32 ? 32 : kAccStages * kAccCols;
   // barriers + ring + scalars + expert tables
   static constexpr int kAuxBytes = 8 * (2 * kStages + 2 * kAccStages + 2 * kRing) + 16 * kRing + 16 +
-                                   4 * (3 * kMaxExperts + 2) + 4 * MAX_N;
+                                   4 * (3 * kMaxExperts + 2) + 4 * MAX_N + 4 * (kEpiThreads + 4);
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
 };
 
 enum : int { kItemUp = 0, kItemDown = 1, kItemEnd = 2 };
 
-__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+// SiLU(g) * u with one MUFU op: silu(g) = 0.5 g (1 + tanh(g / 2)); tanh.approx
+// (rel. err ~2^-11) is well below the bf16 rounding of the result.
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  const float hg = 0.5f * g;
+  return fmaf(hg, tanh_approx(hg), hg) * u;
+}
 
 // GATHER: UP items read token rows of an unpermuted [rows, H] source through
 // TMA tile::gather4 (tok_of indices); otherwise rows are expert-contiguous
@@ -95,6 +191,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   int32_t* s_tp = s_off + (kMaxExperts + 1);
   int32_t* s_ts = s_tp + (kMaxExperts + 1);
   int32_t* s_tok = s_ts + kMaxExperts;  // [MAX_N] source rows of the current UP item
+  int32_t* s_fin = s_tok + MAX_N;       // [kEpiThreads] tokens whose block this DN item completed; [.. + 0] count
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
@@ -103,7 +200,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiThreads); }
     for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], 2); }
     fence_mbar_init();
   }
@@ -141,7 +238,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
 
   if (warp == 0) {
     // ===================== scheduler + TMA producer (warp-wide) =====================
-    const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+    const uint64_t pol_w = p.weights_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_a = policy_evict_last();   // activations: re-read by every m-tile
     int stage = 0; uint32_t phase = 0;
     int r = 0; uint32_t rph = 0;
@@ -219,6 +316,16 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + 2 * kATileBytes;
           mbar_arrive_expect_tx(&full[stage], bytes);
+          if (p.lookahead && kb + p.lookahead < kblocks) {  // warm L2 ahead of the ring
+            const int kp = (kb + p.lookahead) * kTileK;
+            if (up) {
+              tma_prefetch_2d(&tm_w13, kp, arow);
+              tma_prefetch_2d(&tm_w13, kp, arow + p.I);
+            } else {
+              tma_prefetch_2d(&tm_w2, kp, arow);
+              if (two) tma_prefetch_2d(&tm_w2, kp, arow + kTileM);
+            }
+          }
           if (up) {
             tma_load_2d(sa, &tm_w13, &full[stage], kb * kTileK, arow, pol_w);
             tma_load_2d(sa + kATileBytes, &tm_w13, &full[stage], kb * kTileK, arow + p.I, pol_w);
@@ -287,8 +394,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs -> global =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int et = threadIdx.x - 128;
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;       // 0: even chunks, 1: odd chunks
+    const int et = threadIdx.x - 128;       // 0..255
     int r = 0; uint32_t rph = 0;
     int acc = 0; uint32_t aph = 0;
     while (true) {
@@ -304,7 +412,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       const int nchunks = (nvalid + 15) / 16;
       if (kind == kItemUp) {
         __nv_bfloat16* dst = p.act + static_cast<size_t>(row0) * p.I + feat;
-        for (int c = 0; c < nchunks; ++c) {
+        for (int c = half; c < nchunks; c += 2) {
           uint32_t g[16], u[16];
           tmem_ld16(t_gate + c * 16, g);
           tmem_ld16(t_gate + MAX_N + c * 16, u);
@@ -320,7 +428,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       } else {
         const bool two = m0 + kTileM < p.H;
         __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
-        for (int c = 0; c < nchunks; ++c) {
+        for (int c = half; c < nchunks; c += 2) {
           uint32_t v[16], v2[16];
           tmem_ld16(t_gate + c * 16, v);
           if (two) tmem_ld16(t_gate + MAX_N + c * 16, v2);
@@ -338,14 +446,14 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == A_) { acc = 0; aph ^= 1; }
-      if (kind == kItemUp) {
-        fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
-        __threadfence();
-      }
-      named_bar_sync(1, 128);
+      if (kind == kItemUp) fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
+      if (kind == kItemDown && p.y != nullptr) fused_combine(p, m0, row0, nvalid, et, s_fin);
       if (et == 0) {
         mbar_arrive(&sempty[r]);
-        if (kind == kItemUp) atomicAdd(&p.sched[1 + e], 1u);
+        if (kind == kItemUp) {  // release: every epilogue thread's act stores precede the count
+          __threadfence();
+          atomicAdd(&p.sched[1 + e], 1u);
+        }
       }
       if (++r == kRing) { r = 0; rph ^= 1; }
     }

@@ -61,7 +61,19 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ------------------------------------------------------------------ shapes
+// Tuning knobs read once from the environment (experiments only; defaults are the product).
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+bool use_pdl() {
+  static const bool v = env_int("LPMOE_PDL", 1) != 0;
+  return v;
+}
+
 int pick_max_n(int S, int E) {
+  static const int forced = env_int("LPMOE_MAX_N", 0);
+  if (forced == 64 || forced == 128 || forced == 256) return forced;
   const int avg = (S + E - 1) / E;
   if (avg <= 40) return 64;
   if (avg <= 96) return 128;
@@ -78,24 +90,42 @@ constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E
 
 struct Layout {
   size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
-  size_t tile_prefix, tile_rows, sched, x_perm, act, y_perm, total;
+  size_t tile_prefix, tile_rows, sched, blk_cnt, x_perm, act, y_perm, total;
+  int blk_n;  // fused-combine counters: T * ceil(H/256)
   int csize;         // router cluster size
   int chunk_tokens;  // tokens per permutation chunk (= router tile)
   int nchunks;
 };
 
+// Router tile (tokens per MMA N = permutation chunk): 16 while the batch is
+// small (many CTAs, latency-bound), 64 once 16-token tiles would make every
+// one of >= kRouterLargeTiles CTAs re-stream all of Wr from L2.
+constexpr int kRouterLargeTiles = 256;
+int router_tile_tokens(int T, int E, int topk) {
+  static const int forced = env_int("LPMOE_ROUTER_TN", 0);
+  if (forced == 16 || forced == 64) return (forced == 64 && topk > 8) ? 16 : forced;
+  if (topk > 8 || E > 256) return lp::kRouterN;
+  return (T + lp::kRouterN - 1) / lp::kRouterN >= kRouterLargeTiles ? lp::kRouterTileLarge : lp::kRouterN;
+}
+
 // CTAs per router token tile: split H across a cluster while the grid is small.
-int router_cluster(int ntiles, int H) {
+int router_cluster(int ntiles, int H, int TN, int E) {
   int cs = 1;
-  while (cs < 4 && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) cs *= 2;
+  const int cs_max = TN == lp::kRouterTileLarge ? 2 : 4;
+  while (cs < cs_max && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) {
+    const int e_pad = (E + 31) / 32 * 32;
+    const int ppc = 4 / (cs * 2);  // partial sums per CTA after doubling (npart <= 4)
+    if (ppc * TN * e_pad > lp::router_part_floats() || (TN / (cs * 2)) < 4) break;
+    cs *= 2;
+  }
   return cs;
 }
 
 Layout make_layout(int T, int H, int I, int E, int topk) {
   Layout L{};
   const size_t S = static_cast<size_t>(T) * topk;
-  L.csize = router_cluster((T + lp::kRouterN - 1) / lp::kRouterN, H);
-  L.chunk_tokens = lp::kRouterN;
+  L.chunk_tokens = router_tile_tokens(T, E, topk);
+  L.csize = router_cluster((T + L.chunk_tokens - 1) / L.chunk_tokens, H, L.chunk_tokens, E);
   L.nchunks = (T + L.chunk_tokens - 1) / L.chunk_tokens;
   size_t o = kHeaderBytes;
   auto take = [&](size_t bytes) {
@@ -117,6 +147,8 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
   L.x_perm = take(S * H * 2);
   L.act = take(S * I * 2);
   L.y_perm = take(S * H * 2);
+  L.blk_n = T * ((H + 255) / 256);
+  L.blk_cnt = take(static_cast<size_t>(L.blk_n) * 4);
   L.total = o;
   return L;
 }
@@ -188,7 +220,7 @@ cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
   int n = 1;
   if (cluster > 1) {
     attr[1].id = cudaLaunchAttributeClusterDimension;
@@ -216,43 +248,50 @@ int set_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------ stages
-template <int CS, int NV>
+template <int CS, int NV, int TN>
 int launch_router_t(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
                     cudaStream_t st) {
   int rc;
-  const int smem = lp::router_smem_bytes(rp.mtiles);
-  if ((rc = set_smem(lp::k_router<CS, NV>, smem))) return rc;
-  LP_CUDA(launch_pdl_cluster(lp::k_router<CS, NV>, ntiles * CS, lp::kRouterThreads, smem, st, CS, tm_wr, tm_x, rp));
+  const int smem = lp::router_smem_bytes(rp.mtiles, TN);
+  if ((rc = set_smem(lp::k_router<CS, NV, TN>, smem))) return rc;
+  LP_CUDA(launch_pdl_cluster(lp::k_router<CS, NV, TN>, ntiles * CS, lp::router_threads(TN), smem, st, CS, tm_wr, tm_x,
+                             rp));
   return LP_OK;
 }
 
-template <int CS>
+template <int CS, int TN>
 int launch_router_cs(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
                      int e_pad, cudaStream_t st) {
-  constexpr int LPT = 8 * CS;  // lanes per token
+  constexpr int TPC = TN / CS;
+  constexpr int LPT = (128 / TPC) > 8 ? (128 / TPC) : 8;  // lanes per token (route.cuh)
   const int nv = (e_pad + LPT - 1) / LPT;
-  if (nv <= 4) return launch_router_t<CS, 4>(tm_wr, tm_x, rp, ntiles, st);
-  if (nv <= 8) return launch_router_t<CS, 8>(tm_wr, tm_x, rp, ntiles, st);
-  if (nv <= 16) return launch_router_t<CS, 16>(tm_wr, tm_x, rp, ntiles, st);
-  return launch_router_t<CS, 32>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 4) return launch_router_t<CS, 4, TN>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 8) return launch_router_t<CS, 8, TN>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 16) return launch_router_t<CS, 16, TN>(tm_wr, tm_x, rp, ntiles, st);
+  return launch_router_t<CS, 32, TN>(tm_wr, tm_x, rp, ntiles, st);
 }
 
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
                  void* ws, const Layout& L, cudaStream_t st) {
   int rc;
   if ((rc = get_encode())) return rc;
+  const int TN = L.chunk_tokens;
   CUtensorMap tm_wr, tm_x;
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
-  if ((rc = make_tmap(&tm_x, x, T, H, lp::kRouterN))) return rc;
+  if ((rc = make_tmap(&tm_x, x, T, H, TN))) return rc;
   const int mtiles = (E + 127) / 128;
   lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
-  const int ntiles = (T + lp::kRouterN - 1) / lp::kRouterN;
+  const int ntiles = (T + TN - 1) / TN;
   const int e_pad = (E + 31) / 32 * 32;
+  if (TN == lp::kRouterTileLarge) {
+    if (L.csize == 2) return launch_router_cs<2, lp::kRouterTileLarge>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    return launch_router_cs<1, lp::kRouterTileLarge>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+  }
   switch (L.csize) {
-    case 4: return launch_router_cs<4>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-    case 2: return launch_router_cs<2>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-    default: return launch_router_cs<1>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    case 4: return launch_router_cs<4, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    case 2: return launch_router_cs<2, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    default: return launch_router_cs<1, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
   }
 }
 
@@ -262,7 +301,8 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
 int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, int topk, int chunk_tokens,
                         int32_t* counts, int32_t* offsets, int32_t* slot_of, int32_t* tok_of, void* x_perm,
                         int32_t* chunk_hist, const int32_t* rank_local, int max_n, int32_t* tile_prefix,
-                        int32_t* tile_rows, uint32_t* sched, cudaStream_t st) {
+                        int32_t* tile_rows, uint32_t* sched, cudaStream_t st, uint32_t* zero_buf = nullptr,
+                        int zero_n = 0) {
   const int S = T * topk;
   const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
   const int n_hist = nchunks * E;
@@ -272,7 +312,7 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
     if ((rc = set_smem(lp::k_scan, lp::kScanSmemInts * 4))) return rc;
   }
   LP_CUDA(launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts, offsets,
-                     tile_prefix, tile_rows, sched));
+                     tile_prefix, tile_rows, sched, zero_buf, zero_n));
   LP_CUDA(launch_pdl(lp::k_scatter, (S + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
                      static_cast<const int32_t*>(offsets), static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
                      chunk_tokens * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
@@ -306,13 +346,44 @@ int prefetch_kblocks() {
   return v;
 }
 
+bool use_gather(int T) {
+  static const int v = env_int("LPMOE_GATHER", 0);  // 0 off, 1 on, >1: on from T >= v
+  return v == 1 || (v > 1 && T >= v);
+}
+int env_lookahead() {
+  static const int v = env_int("LPMOE_LOOKAHEAD", 0);
+  return v;
+}
+int env_wpol() {
+  static const int v = env_int("LPMOE_WEVICT_FIRST", 1);
+  return v;
+}
+
+// Optional combine fused into the expert kernel's DN epilogue (experts_sm100.cuh).
+struct FusedCombine {
+  void* y = nullptr;
+  const int32_t* slot_tok = nullptr;
+  const int32_t* slot_of = nullptr;
+  const float* wgt = nullptr;
+  uint32_t* blk_cnt = nullptr;
+  int topk = 0;
+};
+bool use_fused_combine() {
+  // Off by default: measured slower on B200 (the DN epilogue is on the critical
+  // path: +10 us at T=576, +140 us at T=8224 vs the separate k_combine).
+  static const bool v = env_int("LPMOE_FUSED_COMBINE", 0) != 0;
+  return v;
+}
+
 // src: [src_rows, H] token rows; slot s reads row tok_of[s] (tok_of == nullptr: row s).
 int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, const void* w13, const void* w2,
                    int H, int I, int E, int max_n, const int32_t* offsets, const int32_t* tile_prefix,
-                   const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st) {
+                   const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st,
+                   const FusedCombine& fc = FusedCombine{}) {
   lp::ExpertsParams p{H,       I,           E,        tok_of, offsets, tile_prefix, tile_rows,
                       static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                      prefetch_kblocks()};
+                      prefetch_kblocks(), env_lookahead(), env_wpol(), static_cast<__nv_bfloat16*>(fc.y),
+                      fc.slot_tok, fc.slot_of, fc.wgt, fc.blk_cnt, fc.topk};
   if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
     switch (max_n) {
       case 64: return launch_experts_t<64, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
@@ -477,20 +548,28 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
   prof_mark(1, st);
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
+  // Token rows reach the expert kernel either materialised in slot order
+  // (x_perm, one scatter pass) or gathered straight from x by TMA (tok_of).
+  const bool gather = use_gather(T);
+  const bool fused = use_fused_combine();
   if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
-                                at<void>(ws, L.x_perm),
+                                gather ? nullptr : at<void>(ws, L.x_perm),
                                 at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
                                 at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
-                                at<uint32_t>(ws, L.sched), st)))
+                                at<uint32_t>(ws, L.sched), st, fused ? at<uint32_t>(ws, L.blk_cnt) : nullptr,
+                                fused ? L.blk_n : 0)))
     return rc;
+  FusedCombine fc;
+  if (fused) fc = FusedCombine{y, tok_of, slot_of, w, at<uint32_t>(ws, L.blk_cnt), topk};
   prof_mark(2, st);
-  if ((rc = launch_experts(at<void>(ws, L.x_perm), S, nullptr, S, w13, w2, H, I, E, max_n, offsets,
+  if ((rc = launch_experts(gather ? x : at<void>(ws, L.x_perm), gather ? T : S, gather ? tok_of : nullptr, S, w13,
+                           w2, H, I, E, max_n, offsets,
                            at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
-                           at<void>(ws, L.y_perm), st)))
+                           at<void>(ws, L.y_perm), st, fc)))
     return rc;
   prof_mark(3, st);
-  if ((rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;
+  if (!fused && (rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;
   prof_mark(4, st);
   return ok();
 }

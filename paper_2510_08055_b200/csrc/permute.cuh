@@ -70,7 +70,7 @@ constexpr int kScanSmemInts = 24576;  // 96 KiB
 __global__ void __launch_bounds__(kScanThreads)
     k_scan(int32_t* __restrict__ chunk_hist, int nchunks, int E, int max_n, int32_t* __restrict__ counts,
            int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
-           uint32_t* __restrict__ sched) {
+           uint32_t* __restrict__ sched, uint32_t* __restrict__ zero_buf, int zero_n) {
   extern __shared__ int32_t s_hist[];
   __shared__ int32_t s_part[kScanThreads];
   __shared__ int32_t s_cnt[256];
@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(kScanThreads)
     }
   }
   for (int i = tid; i <= E; i += kScanThreads) sched[i] = 0u;
+  // fused-combine counters of the expert kernel start from zero (256-B aligned region)
+  for (int i = tid; i < zero_n / 4; i += kScanThreads) reinterpret_cast<uint4*>(zero_buf)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = (zero_n / 4) * 4 + tid; i < zero_n; i += kScanThreads) zero_buf[i] = 0u;
   if (!staged) return;
   // staged path: the per-tile bases live in smem; publish them for the scatter
   __syncthreads();

@@ -27,14 +27,12 @@
 
 namespace lp {
 
-constexpr int kRouterN = 16;         // tokens per router tile (= permutation chunk)
+constexpr int kRouterN = 16;         // tokens per router tile for small batches (= permutation chunk)
 constexpr int kRouterStages = 6;
-constexpr int kRouterThreads = 192;  // w0 TMA, w1 MMA + TMEM, w2..w5 epilogue
-constexpr int kRouterBBytes = kRouterN * 128;
-constexpr int kRouterTmemCols = 128;  // 4 partial sums x 2 m-tiles x 16 tokens
-__host__ __device__ constexpr int router_smem_bytes(int mtiles) {
-  return 1024 + kRouterStages * (mtiles * 16384 + kRouterBBytes) + 256;
-}
+// w0 TMA, w1 MMA + TMEM, w2..w5 TMEM drain + histogram, w2.. top-k. Large
+// tiles gate 64 tokens per CTA: the latency-bound top-k gets 10 warps.
+__host__ __device__ constexpr int router_threads(int TN) { return TN >= 64 ? 384 : 192; }
+constexpr int kRouterTileLarge = 64;  // tokens per tile for large batches (fewer Wr re-reads)
 
 struct RouterParams {
   int T, H, E, topk, renorm;
@@ -63,9 +61,10 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
   for (int o = 1; o < LPT; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float ssum = 0.f;
 #pragma unroll
-  for (int j = 0; j < NV; ++j) ssum += (l[j] == -INFINITY) ? 0.f : expf(l[j] - m);
+  for (int j = 0; j < NV; ++j) ssum += (l[j] == -INFINITY) ? 0.f : __expf(l[j] - m);
 #pragma unroll
   for (int o = 1; o < LPT; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  const float inv = 1.0f / ssum;
   uint32_t taken = 0;
   psum = 0.f;
   if constexpr (LPT == 32) {
@@ -83,7 +82,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
       const int bi = static_cast<int>(__reduce_min_sync(0xffffffffu, cand));
       if ((bi & 31) == sub) taken |= 1u << (bi >> 5);
       const uint32_t vb = (kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax;
-      const float pr = expf(__uint_as_float(vb) - m) / ssum;
+      const float pr = __expf(__uint_as_float(vb) - m) * inv;
       psum += pr;
       if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
     }
@@ -105,32 +104,54 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
       }
     }
     if (bi % LPT == sub) taken |= 1u << (bi / LPT);
-    const float pr = expf(bv - m) / ssum;
+    const float pr = __expf(bv - m) * inv;
     psum += pr;
     if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
   }
 }
 
-// CS: cluster size (CTAs per token tile); NV: logits per lane in the top-k.
-template <int CS, int NV>
-__global__ void __launch_bounds__(kRouterThreads, 1)
+// Shared-memory plan of one router CTA: the TMA ring during the K loop, then
+// (aliased, once every MMA has drained it) the epilogue scratch.
+__host__ __device__ constexpr int router_ring_bytes(int mtiles, int TN) {
+  return kRouterStages * (mtiles * 16384 + TN * 128);
+}
+__host__ __device__ constexpr int router_part_floats() { return 4 * 16 * 256; }  // 64 KiB: cluster partials
+__host__ __device__ constexpr int router_scratch_bytes(int TN) {
+  // partials | logits [TN][256] | ids, p [TN][32] | 4 warp hists + cta + base [7][256] | ranks, experts [128][4]
+  return 4 * (router_part_floats() + TN * 256 + 2 * TN * 32 + 7 * 256 + 2 * 512);
+}
+__host__ __device__ constexpr int router_smem_bytes(int mtiles, int TN) {
+  return 1024 + (router_ring_bytes(mtiles, TN) > router_scratch_bytes(TN) ? router_ring_bytes(mtiles, TN)
+                                                                           : router_scratch_bytes(TN)) +
+         256;
+}
+
+// CS: cluster size (CTAs per token tile); NV: logits per lane in the top-k;
+// TN: tokens per tile (MMA N, = the permutation chunk). LPT lanes gate one
+// token, so the 128 epilogue threads take 128/LPT tokens per round.
+template <int CS, int NV, int TN>
+__global__ void __launch_bounds__(router_threads(TN), 1)
     k_router(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const RouterParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int stage_bytes = p.mtiles * 16384 + kRouterBBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStages * stage_bytes);
+  const int stage_bytes = p.mtiles * 16384 + TN * 128;
+  const int ring = router_ring_bytes(p.mtiles, TN);
+  const int scratch = router_scratch_bytes(TN);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (ring > scratch ? ring : scratch));
   uint64_t* empty = full + kRouterStages;
   uint64_t* tfull = empty + kRouterStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = warp_idx();
   const int lane = threadIdx.x & 31;
-  constexpr int TPC = kRouterN / CS;  // tokens this CTA gates (its permutation chunk)
-  constexpr int LPT = 128 / TPC;      // lanes per token in the top-k
+  constexpr int kRouterGate = router_threads(TN) - 64;  // threads gating tokens
+  constexpr int TPC = TN / CS;                    // tokens this CTA gates
+  constexpr int LPT = (128 / TPC) > 8 ? (128 / TPC) : 8;  // lanes per token in the top-k
+  constexpr int TMEM_COLS = 4 * 2 * TN <= 32 ? 32 : (4 * 2 * TN <= 128 ? 128 : (4 * 2 * TN <= 256 ? 256 : 512));
   const int cr = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int tile = blockIdx.x / CS;
-  const int t0 = tile * kRouterN;
+  const int t0 = tile * TN;
   // K = H is summed as NPART fixed partial sums (each a separate TMEM
   // accumulator, folded left in part order), whatever the cluster size: the
   // fp32 logits of a token are then bit-identical for every batch size and
@@ -151,7 +172,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     prefetch_tmap(&tm_wr);
     prefetch_tmap(&tm_x);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kRouterTmemCols);
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
@@ -161,15 +182,15 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   if (threadIdx.x == 0) LP_TRACE_AT(tr, 1);
 
   const int e_pad = (p.E + 31) & ~31;
-  float* s_part = reinterpret_cast<float*>(smem);             // [ppc][kRouterN][e_pad] this CTA's partial logits
-  float* s_logit = s_part + 4 * kRouterN * 256;                // [TPC][e_pad] this CTA's token logits
-  int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + kRouterN * 256);  // [kRouterN][32]
-  float* s_p = reinterpret_cast<float*>(s_ids + kRouterN * 32);          // [kRouterN][32]
-  int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + kRouterN * 32);       // [4][e_pad]
-  int32_t* s_cta = s_wh + 4 * 256;                                        // [e_pad] this CTA's chunk totals
-  int32_t* s_base = s_cta + 256;                                          // [e_pad] totals of lower ranks
-  int32_t* s_rank = s_base + 256;                                         // [128][4] in-warp ranks
-  int32_t* s_ent = s_rank + 512;                                          // [128][4] entry experts
+  float* s_part = reinterpret_cast<float*>(smem);                 // [ppc][TN][e_pad] partial logits (CS > 1)
+  float* s_logit = s_part + router_part_floats();                  // [TPC][e_pad] this CTA's token logits
+  int32_t* s_ids = reinterpret_cast<int32_t*>(s_logit + TN * 256);  // [TN][32]
+  float* s_p = reinterpret_cast<float*>(s_ids + TN * 32);           // [TN][32]
+  int32_t* s_wh = reinterpret_cast<int32_t*>(s_p + TN * 32);        // [4][e_pad]
+  int32_t* s_cta = s_wh + 4 * 256;                                 // [e_pad] this CTA's chunk totals
+  int32_t* s_base = s_cta + 256;                                   // [e_pad] totals of lower ranks
+  int32_t* s_rank = s_base + 256;                                  // [128][4] in-warp ranks
+  int32_t* s_ent = s_rank + 512;                                   // [128][4] entry experts
 
   if (warp == 0) {
     if (lane == 0) {
@@ -188,26 +209,26 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, kRouterN);
+      constexpr uint32_t idesc = idesc_bf16_f32(128, TN);
       for (int i = 0; i < kb_per; ++i) {
         const int s = i % kRouterStages;
         mbar_wait(&full[s], (i / kRouterStages) & 1);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * stage_bytes);
         const uint64_t b = sdesc_kmajor_sw128(sa + p.mtiles * 16384);
-        const uint32_t d0 = tmem_base + (i / kb_part) * (p.mtiles * kRouterN);
+        const uint32_t d0 = tmem_base + (i / kb_part) * (p.mtiles * TN);
         for (int mt = 0; mt < p.mtiles; ++mt) {
           const uint64_t a = sdesc_kmajor_sw128(sa + mt * 16384);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16(d0 + mt * kRouterN, a + 2 * k, b + 2 * k, idesc, ((i % kb_part) | k) != 0);
+            mma_bf16(d0 + mt * TN, a + 2 * k, b + 2 * k, idesc, ((i % kb_part) | k) != 0);
         }
         mma_commit(&empty[s]);
       }
       mma_commit(tfull);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // TMEM -> smem (the ring is drained once tfull fires: every MMA has read its stage)
     const int q = warp & 3;
     mbar_wait(tfull, 0);
@@ -215,24 +236,26 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     if (threadIdx.x == 64) LP_TRACE_AT(tr, 4);
     for (int mt = 0; mt < p.mtiles; ++mt) {
       const int e = mt * 128 + 32 * q + lane;
-      float acc[kRouterN];
-      for (int pl = 0; pl < ppc; ++pl) {
-        uint32_t v[16];
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (pl * p.mtiles + mt) * kRouterN, v);
-        tmem_wait_ld();
-        if (CS > 1) {  // parked for the cluster-wide fold below
-          if (e < e_pad) {
+      for (int c = 0; c < TN / 16; ++c) {
+        float acc[16];
+        for (int pl = 0; pl < ppc; ++pl) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (pl * p.mtiles + mt) * TN + c * 16, v);
+          tmem_wait_ld();
+          if (CS > 1) {  // parked for the cluster-wide fold below
+            if (e < e_pad) {
 #pragma unroll
-            for (int i = 0; i < kRouterN; ++i) s_part[(pl * kRouterN + i) * e_pad + e] = __uint_as_float(v[i]);
+              for (int i = 0; i < 16; ++i) s_part[(pl * TN + c * 16 + i) * e_pad + e] = __uint_as_float(v[i]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = pl ? acc[i] + __uint_as_float(v[i]) : __uint_as_float(v[i]);
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < kRouterN; ++i) acc[i] = pl ? acc[i] + __uint_as_float(v[i]) : __uint_as_float(v[i]);
         }
-      }
-      if (CS == 1 && e < e_pad) {
+        if (CS == 1 && e < e_pad) {
 #pragma unroll
-        for (int i = 0; i < kRouterN; ++i) s_logit[i * e_pad + e] = acc[i];
+          for (int i = 0; i < 16; ++i) s_logit[(c * 16 + i) * e_pad + e] = acc[i];
+        }
       }
     }
   }
@@ -243,16 +266,16 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     cluster_sync();  // every CTA's partial logits are now readable over DSMEM
     if (threadIdx.x == 0) LP_TRACE_AT(tr, 11);
     if (warp >= 2) {
-      // this CTA's token rows: s_logit[i][e] = sum_rank partial_rank[cr*TPC + i][e] (rank order)
+      // this CTA's token rows: s_logit[i][e] = fold over global part order (rank r, local part pl)
       const int et = threadIdx.x - 64;
       const int nq = TPC * (e_pad / 4);
-      for (int idx = et; idx < nq; idx += 128) {
+      for (int idx = et; idx < nq; idx += kRouterGate) {
         const int off = cr * TPC * e_pad + idx * 4;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < CS; ++r) {
-          for (int pl = 0; pl < ppc; ++pl) {  // global part order r*ppc + pl
-            const float4 v = ld_dsmem_f4(mapa_shared(smem_u32(s_part + pl * kRouterN * e_pad + off), r));
+          for (int pl = 0; pl < ppc; ++pl) {
+            const float4 v = ld_dsmem_f4(mapa_shared(smem_u32(s_part + pl * TN * e_pad + off), r));
             if (r == 0 && pl == 0) {
               acc = v;
             } else {
@@ -267,33 +290,41 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     if (threadIdx.x == 0) LP_TRACE_AT(tr, 12);
   }
   if (warp >= 2) {
-    const int q = warp & 3;
-    const int et = threadIdx.x - 64;  // 0..127
+    // ---------------- softmax + top-k: LPT lanes per token, all gating warps ----------------
+    const int tk = threadIdx.x - 64;  // 0..kRouterGate-1
     const int tc0 = t0 + cr * TPC;   // first token of this CTA's chunk
-    named_bar_sync(1, 128);
-    // ---------------- softmax + top-k: LPT lanes per token ----------------
-    {
-      const int g = et / LPT;
-      const int sub = et % LPT;
-      const int t = tc0 + g;
-      float psum;
-      topk_lanes<LPT, NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
-      named_bar_sync(1, 128);
-      if (t < p.T) {
-        for (int r = sub; r < p.topk; r += LPT) {
-          p.ids[static_cast<size_t>(t) * p.topk + r] = s_ids[g * 32 + r];
-          p.w[static_cast<size_t>(t) * p.topk + r] = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r];
+    named_bar_sync(1, kRouterGate);
+    constexpr int TPRG = (kRouterGate / 32) * (32 / LPT);  // tokens per round (whole warps)
+    for (int g0 = 0; g0 < TPC; g0 += TPRG) {
+      const int g = g0 + tk / LPT;  // warp-uniform bound: TPC is a multiple of 32/LPT
+      if (g < TPC) {
+        const int sub = tk % LPT;
+        const int t = tc0 + g;
+        float psum;
+        topk_lanes<LPT, NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
+        __syncwarp();
+        if (t < p.T) {
+          for (int r = sub; r < p.topk; r += LPT) {
+            p.ids[static_cast<size_t>(t) * p.topk + r] = s_ids[g * 32 + r];
+            p.w[static_cast<size_t>(t) * p.topk + r] = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r];
+          }
         }
       }
     }
-    if (et == 0) LP_TRACE_AT(tr, 5);
+    named_bar_sync(1, kRouterGate);
+    if (tk == 0) LP_TRACE_AT(tr, 5);
+  }
+  if (warp >= 2 && warp < 6) {
+    const int q = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    const int tc0 = t0 + cr * TPC;
     // ---------------- stable chunk histogram + ranks: warp q owns TPC/4 tokens ----------------
     constexpr int TPW = TPC / 4;
     for (int ee = lane; ee < e_pad; ee += 32) s_wh[q * e_pad + ee] = 0;
     __syncwarp();
     const int tok_lo = q * TPW;
     const int n_tok = max(0, min(TPW, p.T - tc0 - tok_lo));
-    const int n_ent = n_tok * p.topk;
+    const int n_ent = n_tok * p.topk;  // <= 128 (host picks TN so that TPW * topk <= 128)
     const unsigned lt = (1u << lane) - 1u;
     int my_rank[4], my_e[4];
 #pragma unroll
@@ -315,7 +346,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         __syncwarp();
       }
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(2, 128);
     // exclusive scan over this CTA's 4 warps; the CTA's total goes to s_cta[e]
     for (int ee = et; ee < e_pad; ee += 128) {
       int run = 0;
@@ -327,12 +358,9 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       }
       s_cta[ee] = run;
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(2, 128);
     if constexpr (CS == 1) {
       for (int ee = et; ee < p.E; ee += 128) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = s_cta[ee];
-    }
-    // (CS > 1: cross-CTA bases are applied after the cluster barrier below)
-    if constexpr (CS == 1) {
 #pragma unroll
       for (int st = 0; st < 4; ++st) {
         if (my_e[st] >= 0)
@@ -340,6 +368,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
               my_rank[st] + s_wh[q * e_pad + my_e[st]];
       }
     }
+    // (CS > 1: cross-CTA bases are applied after the cluster barrier below)
     for (int st = 0; st < 4; ++st) { s_rank[et * 4 + st] = my_rank[st]; s_ent[et * 4 + st] = my_e[st]; }
   }
   if constexpr (CS > 1) {
@@ -347,7 +376,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     // its ranks; the last CTA writes the tile total. Fixed order -> stable slots.
     __syncthreads();
     cluster_sync();
-    if (warp >= 2) {
+    if (warp >= 2 && warp < 6) {
       const int q = warp & 3;
       const int et = threadIdx.x - 64;
       const int tc0 = t0 + cr * TPC;
@@ -365,7 +394,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         s_base[ee] = before;
         if (cr == CS - 1 && ee < p.E) p.tile_hist[static_cast<size_t>(tile) * p.E + ee] = total;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(2, 128);
 #pragma unroll
       for (int st = 0; st < 4; ++st) {
         const int ex = s_ent[et * 4 + st];
@@ -382,7 +411,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kRouterTmemCols);
+    tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
