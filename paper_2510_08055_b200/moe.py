@@ -207,6 +207,60 @@ class GpuMoE:
         return y
 
 
+class HostPipeline:
+    """End-to-end forwards from pinned host buffers with the copies overlapped.
+
+    Step i's H2D copy runs on an upload stream and step i's D2H copy on a
+    download stream, so while layer i computes, the input of step i+1 is
+    uploading and the output of step i-1 is downloading (PCIe is full duplex).
+    `depth` device staging buffers per direction; every hazard is an event:
+    an upload waits until the compute that last read its staging buffer is
+    done, a compute waits for its upload and for the download that last read
+    its output buffer. Results land in the caller's host tensors in order.
+    """
+
+    def __init__(self, device: torch.device, T: int, H: int, depth: int = 2):
+        self.device, self.depth = device, depth
+        self.up = torch.cuda.Stream(device)
+        self.down = torch.cuda.Stream(device)
+        self.xd = [torch.empty((T, H), dtype=torch.bfloat16, device=device) for _ in range(depth)]
+        self.yd = [torch.empty((T, H), dtype=torch.bfloat16, device=device) for _ in range(depth)]
+        self.ev_up = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_down = [torch.cuda.Event() for _ in range(depth)]
+        self.i = 0
+
+    def start(self, event: torch.cuda.Event) -> None:
+        """Order the first copies after `event` (the start of a timed region)."""
+        self.up.wait_event(event)
+        self.down.wait_event(event)
+
+    def submit(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> MoEStats:
+        require(not x_host.is_cuda and not y_host.is_cuda, "HostPipeline.submit expects host tensors")
+        b = self.i % self.depth
+        self.i += 1
+        comp = torch.cuda.current_stream(self.device)
+        self.up.wait_event(self.ev_comp[b])          # staging buffer b no longer read by compute
+        with torch.cuda.stream(self.up):
+            self.xd[b].copy_(x_host, non_blocking=True)
+            self.ev_up[b].record(self.up)
+        comp.wait_event(self.ev_up[b])
+        comp.wait_event(self.ev_down[b])              # output buffer b downloaded
+        _, stats = layer.forward(self.xd[b], out=self.yd[b])
+        self.ev_comp[b].record(comp)
+        self.down.wait_event(self.ev_comp[b])
+        with torch.cuda.stream(self.down):
+            y_host.copy_(self.yd[b], non_blocking=True)
+            self.ev_down[b].record(self.down)
+        return stats
+
+    def drain(self) -> None:
+        """Make the current stream wait for every submitted download."""
+        comp = torch.cuda.current_stream(self.device)
+        for e in self.ev_down:
+            comp.wait_event(e)
+
+
 def layer_from_seed(shape: MoEShape, seed: int, device: str = "cuda", tie_break: bool = True) -> GpuMoE:
     """Random-init layer on the dyadic router grid (see synthetic.py)."""
     from .synthetic import expert_weights, router_weight

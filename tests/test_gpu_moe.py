@@ -196,3 +196,23 @@ def test_add_rmsnorm_matches_torch(cuda, T, with_delta):
     ref = hf * torch.rsqrt(hf.pow(2).mean(dim=1, keepdim=True) + 1e-6)
     err = (xn.cpu().float() - ref).norm() / ref.norm()
     assert err < 4e-3, err
+
+
+def test_host_pipeline_matches_device_forward(cuda):
+    """Overlapped H2D / compute / D2H (HostPipeline) returns exactly the device forward's outputs, in order."""
+    from paper_2510_08055_b200.moe import HostPipeline
+
+    s = QWEN3_30B_A3B
+    _, _, _, layer = make(s, 0, cuda)
+    T = 96
+    xs = [router_tokens(T, s.hidden, 100 + i).pin_memory() for i in range(5)]
+    ys = [torch.empty((T, s.hidden), dtype=torch.bfloat16).pin_memory() for _ in range(5)]
+    pipe = HostPipeline(cuda, T, s.hidden)
+    for x, y in zip(xs, ys):
+        pipe.submit(layer, x, y)
+    pipe.drain()
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        ref, _ = layer(x.to(cuda))
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref.cpu())
