@@ -83,7 +83,7 @@ int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, i
                    void* stream);
 
 /* K1..K4 in one call: y [T,H] bf16 = MoE(x). ids / w / counts may be NULL
- * (kept in the workspace). Replaces the pair
+ * (kept in the workspace); T == 0 only zero-fills counts (if given). Replaces the pair
  * `coverage_model.coverage(routed)` + `moe_cost(model, routed, cov, 1)` at
  * engine.py:147-148 / :152-153 with the real layer. */
 int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w2, int T, int H, int I, int E,

@@ -87,6 +87,7 @@ constexpr int kMaxTokens = 262144;
 constexpr size_t kTicketOff = 0;
 constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB of tickets
 constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E+1 <= 257)
+constexpr size_t kGbarOff = kSchedOff + 2048;                // fused router grid barrier (2 words)
 
 struct Layout {
   size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
@@ -100,7 +101,7 @@ struct Layout {
 // Router tile (tokens per MMA N = permutation chunk): 16 while the batch is
 // small (many CTAs, latency-bound), 64 once 16-token tiles would make every
 // one of >= kRouterLargeTiles CTAs re-stream all of Wr from L2.
-constexpr int kRouterLargeTiles = 256;
+constexpr int kRouterLargeTiles = 149;  // > one wave of 16-token tiles on 148 SMs
 int router_tile_tokens(int T, int E, int topk) {
   static const int forced = env_int("LPMOE_ROUTER_TN", 0);
   if (forced == 16 || forced == 64) return (forced == 64 && topk > 8) ? 16 : forced;
@@ -248,31 +249,72 @@ int set_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------ stages
-template <int CS, int NV, int TN>
+template <int CS, int NV, int TN, bool FUSED>
 int launch_router_t(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
                     cudaStream_t st) {
   int rc;
   const int smem = lp::router_smem_bytes(rp.mtiles, TN);
-  if ((rc = set_smem(lp::k_router<CS, NV, TN>, smem))) return rc;
-  LP_CUDA(launch_pdl_cluster(lp::k_router<CS, NV, TN>, ntiles * CS, lp::router_threads(TN), smem, st, CS, tm_wr, tm_x,
-                             rp));
+  if ((rc = set_smem(lp::k_router<CS, NV, TN, FUSED>, smem))) return rc;
+  LP_CUDA(launch_pdl_cluster(lp::k_router<CS, NV, TN, FUSED>, ntiles * CS, lp::router_threads(TN), smem, st, CS,
+                             tm_wr, tm_x, rp));
   return LP_OK;
 }
 
-template <int CS, int TN>
+template <int CS, int TN, bool FUSED>
 int launch_router_cs(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp, int ntiles,
                      int e_pad, cudaStream_t st) {
   constexpr int TPC = TN / CS;
   constexpr int LPT = (128 / TPC) > 8 ? (128 / TPC) : 8;  // lanes per token (route.cuh)
   const int nv = (e_pad + LPT - 1) / LPT;
-  if (nv <= 4) return launch_router_t<CS, 4, TN>(tm_wr, tm_x, rp, ntiles, st);
-  if (nv <= 8) return launch_router_t<CS, 8, TN>(tm_wr, tm_x, rp, ntiles, st);
-  if (nv <= 16) return launch_router_t<CS, 16, TN>(tm_wr, tm_x, rp, ntiles, st);
-  return launch_router_t<CS, 32, TN>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 4) return launch_router_t<CS, 4, TN, FUSED>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 8) return launch_router_t<CS, 8, TN, FUSED>(tm_wr, tm_x, rp, ntiles, st);
+  if (nv <= 16) return launch_router_t<CS, 16, TN, FUSED>(tm_wr, tm_x, rp, ntiles, st);
+  return launch_router_t<CS, 32, TN, FUSED>(tm_wr, tm_x, rp, ntiles, st);
+}
+
+template <bool FUSED>
+int launch_router_dispatch(const CUtensorMap& tm_wr, const CUtensorMap& tm_x, const lp::RouterParams& rp,
+                           int ntiles, int TN, int csize, int e_pad, cudaStream_t st) {
+  if (TN == lp::kRouterTileLarge) {
+    if (csize == 2) return launch_router_cs<2, lp::kRouterTileLarge, FUSED>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    return launch_router_cs<1, lp::kRouterTileLarge, FUSED>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+  }
+  switch (csize) {
+    case 4: return launch_router_cs<4, lp::kRouterN, FUSED>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    case 2: return launch_router_cs<2, lp::kRouterN, FUSED>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+    default: return launch_router_cs<1, lp::kRouterN, FUSED>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+  }
+}
+
+// Fused permutation outputs (router + grid barrier replaces k_scan + k_scatter).
+struct FusedPermute {
+  int32_t* counts;
+  int32_t* offsets;
+  int32_t* slot_of;
+  int32_t* tok_of;
+  void* x_perm;
+  int max_n;
+  int32_t* tile_prefix;
+  int32_t* tile_rows;
+  uint32_t* sched;
+  uint32_t* gbar;
+};
+
+// Whether the router grid may run the permutation itself: every CTA must be
+// co-resident for the grid barrier (<= one CTA per SM).
+bool fused_route_ok(const Layout& L, int T, int E) {
+  // Off by default: on B200 the post-barrier permutation (latency-bound row
+  // copies from <= 148 CTAs) took as long as k_scan + k_scatter (T=576: 228 vs
+  // 224 us per layer; T=8224: 881 vs 870 us). Kept for experiments.
+  static const bool on = env_int("LPMOE_FUSED_ROUTE", 0) != 0;
+  const int TN = L.chunk_tokens;
+  const int grid = (T + TN - 1) / TN * L.csize;
+  const int e_pad = (E + 31) / 32 * 32;
+  return on && grid <= sm_count() && E % 4 == 0 && e_pad / 4 <= lp::router_threads(TN);
 }
 
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
-                 void* ws, const Layout& L, cudaStream_t st) {
+                 void* ws, const Layout& L, cudaStream_t st, const FusedPermute* fp = nullptr) {
   int rc;
   if ((rc = get_encode())) return rc;
   const int TN = L.chunk_tokens;
@@ -280,19 +322,26 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
   if ((rc = make_tmap(&tm_x, x, T, H, TN))) return rc;
   const int mtiles = (E + 127) / 128;
+  const int ntiles = (T + TN - 1) / TN;
   lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
-  const int ntiles = (T + TN - 1) / TN;
+  rp.ntiles = ntiles;
   const int e_pad = (E + 31) / 32 * 32;
-  if (TN == lp::kRouterTileLarge) {
-    if (L.csize == 2) return launch_router_cs<2, lp::kRouterTileLarge>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-    return launch_router_cs<1, lp::kRouterTileLarge>(tm_wr, tm_x, rp, ntiles, e_pad, st);
+  if (fp) {
+    rp.max_n = fp->max_n;
+    rp.counts = fp->counts;
+    rp.offsets = fp->offsets;
+    rp.slot_of = fp->slot_of;
+    rp.tok_of = fp->tok_of;
+    rp.x = static_cast<const __nv_bfloat16*>(x);
+    rp.x_perm = static_cast<__nv_bfloat16*>(fp->x_perm);
+    rp.tile_prefix = fp->tile_prefix;
+    rp.tile_rows = fp->tile_rows;
+    rp.sched = fp->sched;
+    rp.gbar = fp->gbar;
+    return launch_router_dispatch<true>(tm_wr, tm_x, rp, ntiles, TN, L.csize, e_pad, st);
   }
-  switch (L.csize) {
-    case 4: return launch_router_cs<4, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-    case 2: return launch_router_cs<2, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-    default: return launch_router_cs<1, lp::kRouterN>(tm_wr, tm_x, rp, ntiles, e_pad, st);
-  }
+  return launch_router_dispatch<false>(tm_wr, tm_x, rp, ntiles, TN, L.csize, e_pad, st);
 }
 
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
@@ -530,7 +579,10 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
                    void* stream) {
   int rc;
   if ((rc = check_dims(T, H, I, E, topk))) return rc;
-  if (T == 0) return ok();
+  if (T == 0) {  // empty batch: no expert is hit
+    if (counts) LP_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, static_cast<cudaStream_t>(stream)));
+    return ok();
+  }
   if (!x || !wr || !w13 || !w2 || !y || !ws) return fail(LP_EINVAL, "lp_moe_forward: null pointer argument");
   if (!aligned16(x) || !aligned16(wr) || !aligned16(w13) || !aligned16(w2) || !aligned16(y) || !aligned16(ws))
     return fail(LP_EINVAL, "lp_moe_forward: tensors and workspace must be 16-byte aligned");
@@ -544,21 +596,30 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   const int max_n = pick_max_n(S, E);
   int32_t* offsets = at<int32_t>(ws, L.offsets);
   int32_t* slot_of = at<int32_t>(ws, L.slot_of);
-  prof_mark(0, st);
-  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
-  prof_mark(1, st);
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
   // Token rows reach the expert kernel either materialised in slot order
   // (x_perm, one scatter pass) or gathered straight from x by TMA (tok_of).
   const bool gather = use_gather(T);
   const bool fused = use_fused_combine();
-  if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
-                                gather ? nullptr : at<void>(ws, L.x_perm),
-                                at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
-                                at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
-                                at<uint32_t>(ws, L.sched), st, fused ? at<uint32_t>(ws, L.blk_cnt) : nullptr,
-                                fused ? L.blk_n : 0)))
-    return rc;
+  const bool fused_route = !fused && fused_route_ok(L, T, E);
+  prof_mark(0, st);
+  if (fused_route) {  // router + grid barrier + permutation in one launch
+    const FusedPermute fp{counts, offsets, slot_of, tok_of, gather ? nullptr : at<void>(ws, L.x_perm), max_n,
+                          at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched),
+                          at<uint32_t>(ws, kGbarOff)};
+    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, &fp))) return rc;
+    prof_mark(1, st);
+  } else {
+    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
+    prof_mark(1, st);
+    if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
+                                  gather ? nullptr : at<void>(ws, L.x_perm),
+                                  at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
+                                  at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                  at<uint32_t>(ws, L.sched), st, fused ? at<uint32_t>(ws, L.blk_cnt) : nullptr,
+                                  fused ? L.blk_n : 0)))
+      return rc;
+  }
   FusedCombine fc;
   if (fused) fc = FusedCombine{y, tok_of, slot_of, w, at<uint32_t>(ws, L.blk_cnt), topk};
   prof_mark(2, st);

@@ -39,9 +39,39 @@ struct RouterParams {
   int mtiles;           // ceil(E / 128)
   int32_t* ids;         // [T, topk]
   float* w;             // [T, topk]
-  int32_t* tile_hist;   // [ntiles, E] per-tile expert counts (tile = kRouterN tokens)
+  int32_t* tile_hist;   // [ntiles, E] per-tile expert counts (tile = TN tokens)
   int32_t* rank_local;  // [T*topk] rank of the entry among same-expert entries of its tile
+  // ---- fused permutation (FUSED instantiation only; every CTA co-resident) ----
+  int ntiles, max_n;
+  int32_t* counts;        // [E]
+  int32_t* offsets;       // [E+1]
+  int32_t* slot_of;       // [T*topk]
+  int32_t* tok_of;        // [T*topk]
+  const __nv_bfloat16* x; // [T, H] token rows
+  __nv_bfloat16* x_perm;  // [T*topk, H] (nullptr: slot maps only)
+  int32_t* tile_prefix;   // [E+1] expert token-tile schedule for k_experts
+  int32_t* tile_rows;     // [E]
+  uint32_t* sched;        // [E+1] expert scheduler words, reset here
+  uint32_t* gbar;         // [2] grid barrier (arrive, depart); zero on entry, left zero
 };
+
+// Grid-wide barrier for a co-resident grid (<= 1 CTA per SM, checked by the
+// host). Release: __syncthreads + thread 0's gpu-scope fence before arriving;
+// acquire: ld.acquire of the arrive count. The last CTA to depart resets both
+// words, so the workspace header is zero again for the next call.
+__device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&gbar[0], 1u);
+    while (ld_acquire_u32(&gbar[0]) < nblocks) __nanosleep(32);
+    if (atomicAdd(&gbar[1], 1u) == nblocks - 1) {
+      gbar[0] = 0u;
+      gbar[1] = 0u;
+    }
+  }
+  __syncthreads();
+}
 
 // Softmax + top-k of one token held by LPT consecutive lanes (lane `sub` owns
 // experts sub, sub+LPT, ...). Writes the k ids / probabilities to smem.
@@ -129,7 +159,7 @@ __host__ __device__ constexpr int router_smem_bytes(int mtiles, int TN) {
 // CS: cluster size (CTAs per token tile); NV: logits per lane in the top-k;
 // TN: tokens per tile (MMA N, = the permutation chunk). LPT lanes gate one
 // token, so the 128 epilogue threads take 128/LPT tokens per round.
-template <int CS, int NV, int TN>
+template <int CS, int NV, int TN, bool FUSED>
 __global__ void __launch_bounds__(router_threads(TN), 1)
     k_router(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const RouterParams p) {
@@ -408,11 +438,159 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 64) LP_TRACE_AT(tr, 14);
-  if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  if constexpr (FUSED) {
+    // ---------------- permutation (replaces k_scan + k_scatter) ----------------
+    grid_barrier(p.gbar, gridDim.x);  // every tile histogram / rank is published
+    if (threadIdx.x == 0) LP_TRACE_AT(tr, 15);
+    constexpr int NT = router_threads(TN);
+    // expert totals and this tile's base over all tile histograms: int4 per
+    // thread (4 experts), G thread groups split the tile range, 4 rows in flight
+    const int nvec = e_pad / 4;
+    const int G = NT / nvec;
+    int32_t* s_tot = reinterpret_cast<int32_t*>(smem);  // [G][e_pad] partial totals
+    int32_t* s_bas = s_tot + G * e_pad;                  // [G][e_pad] partial tile bases
+    int32_t* s_off = s_bas + G * e_pad;                  // [e_pad + 1] expert offsets
+    int32_t* s_tb = s_off + 260;                         // [e_pad] this tile's base per expert
+    {
+      const int gi = threadIdx.x / nvec, vq = threadIdx.x % nvec;
+      if (gi < G) {
+        const int per = (p.ntiles + G - 1) / G;
+        const int c0 = min(gi * per, p.ntiles), c1 = min(c0 + per, p.ntiles);
+        int4 tot = make_int4(0, 0, 0, 0), bas = make_int4(0, 0, 0, 0);
+        if (vq * 4 < p.E) {
+          const int4* h4 = reinterpret_cast<const int4*>(p.tile_hist) + vq;
+          const int rs = p.E / 4;  // row stride in int4 (E % 4 == 0 on this path)
+          for (int c = c0; c < c1; c += 4) {
+            int4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              v[u] = (c + u < c1) ? __ldcg(h4 + static_cast<size_t>(c + u) * rs) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              tot.x += v[u].x; tot.y += v[u].y; tot.z += v[u].z; tot.w += v[u].w;
+              if (c + u < tile) { bas.x += v[u].x; bas.y += v[u].y; bas.z += v[u].z; bas.w += v[u].w; }
+            }
+          }
+        }
+        reinterpret_cast<int4*>(s_tot + gi * e_pad)[vq] = tot;
+        reinterpret_cast<int4*>(s_bas + gi * e_pad)[vq] = bas;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // expert totals -> exclusive offsets (e_pad <= 256: 8 experts per lane)
+      constexpr int EPL = 8;
+      int v[EPL];
+      int run = 0;
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const int ee = lane * EPL + u;
+        int tot = 0;
+        if (ee < p.E)
+          for (int g = 0; g < G; ++g) tot += s_tot[g * e_pad + ee];
+        v[u] = tot;
+        run += tot;
+      }
+      int inc = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int ex = inc - run;
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const int ee = lane * EPL + u;
+        if (ee < p.E) s_off[ee] = ex;
+        ex += v[u];
+      }
+      if (lane == 31) s_off[p.E] = inc;
+      if (blockIdx.x == 0) {  // the expert tile schedule k_experts consumes (same as k_scan)
+#pragma unroll
+        for (int u = 0; u < EPL; ++u) {
+          const int ee = lane * EPL + u;
+          if (ee < p.E) { p.counts[ee] = v[u]; p.offsets[ee] = s_off[ee]; }
+        }
+        if (lane == 31) p.offsets[p.E] = inc;
+        int nt[EPL], tr_run = 0;
+#pragma unroll
+        for (int u = 0; u < EPL; ++u) {
+          nt[u] = v[u] > 0 ? (v[u] + p.max_n - 1) / p.max_n : 0;
+          tr_run += nt[u];
+        }
+        int tinc = tr_run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, tinc, o);
+          if (lane >= o) tinc += y;
+        }
+        int tex = tinc - tr_run;
+#pragma unroll
+        for (int u = 0; u < EPL; ++u) {
+          const int ee = lane * EPL + u;
+          if (ee < p.E) {
+            p.tile_prefix[ee] = tex;
+            const int rows = nt[u] ? (v[u] + nt[u] - 1) / nt[u] : 0;
+            p.tile_rows[ee] = min(p.max_n, (rows + 15) & ~15);
+          }
+          tex += nt[u];
+        }
+        if (lane == 31) p.tile_prefix[p.E] = tinc;
+      }
+    } else if (warp == 1 && blockIdx.x == 0) {
+      for (int i = lane; i <= p.E; i += 32) p.sched[i] = 0u;
+    }
+    for (int ee = threadIdx.x; ee < p.E; ee += NT) {
+      int b = 0;
+      for (int g = 0; g < G; ++g) b += s_bas[g * e_pad + ee];
+      s_tb[ee] = b;
+    }
+    __syncthreads();
+    // this CTA's routing entries: slot maps and token-row copies (one warp per entry)
+    const int tc0 = t0 + cr * TPC;
+    const int n_tok = max(0, min(TPC, p.T - tc0));
+    const int n_ent = n_tok * p.topk;
+    const size_t i0 = static_cast<size_t>(tc0) * p.topk;
+    for (int k = threadIdx.x; k < n_ent; k += NT) {  // slot maps
+      const int ee = s_ids[(k / p.topk) * 32 + k % p.topk];
+      const int slot = s_off[ee] + s_tb[ee] + __ldcg(p.rank_local + i0 + k);
+      p.slot_of[i0 + k] = slot;
+      p.tok_of[slot] = tc0 + k / p.topk;
+      s_ent[k] = slot;  // (free after the histogram) slot of this CTA's entry k
+    }
+    __syncthreads();
+    if (p.x_perm != nullptr) {  // token-row copies: 2 entries per warp, a whole row per lane batch
+      const int nv = p.H / 8;
+      constexpr int U = 8;
+      for (int k0 = 2 * warp; k0 < n_ent; k0 += 2 * (NT / 32)) {
+        for (int v0 = lane; v0 < nv; v0 += 32 * U) {
+          uint4 r[2][U];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = k0 + h;
+            const uint4* src = reinterpret_cast<const uint4*>(p.x + static_cast<size_t>(tc0 + k / p.topk) * p.H);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (k < n_ent && v0 + 32 * u < nv) r[h][u] = __ldg(src + v0 + 32 * u);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = k0 + h;
+            if (k < n_ent) {
+              uint4* dst = reinterpret_cast<uint4*>(p.x_perm + static_cast<size_t>(s_ent[k]) * p.H);
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (v0 + 32 * u < nv) dst[v0 + 32 * u] = r[h][u];
+            }
+          }
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) { LP_TRACE_AT(tr, 6); LP_TRACE_MAX(9); }
 }
 
 }  // namespace lp

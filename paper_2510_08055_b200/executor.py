@@ -26,7 +26,7 @@ from __future__ import annotations
 import torch
 
 from . import costmodel as cm
-from .moe import GpuMoE, add_rmsnorm
+from .moe import GpuMoE, Workspace, add_rmsnorm
 from .serving import BatchPlan, ServingState, attention_kernels
 from .synthetic import router_weight
 from .types import ModelSpec, MoEShape
@@ -39,13 +39,14 @@ class MoEModel:
         self.shape, self.num_layers = shape, num_layers
         self.device = torch.device(device)
         self.layers: list[GpuMoE] = []
+        self.workspace = Workspace(self.device)  # one scratch for the whole stack (layers run in order)
         for i in range(num_layers):
             g = torch.Generator(device=self.device).manual_seed(seed * 1000 + i)
             E, H, I = shape.num_experts, shape.hidden, shape.ffn
             w13 = (torch.randn((E, 2 * I, H), generator=g, device=self.device) * std).to(torch.bfloat16)
             w2 = (torch.randn((E, H, I), generator=g, device=self.device) * std).to(torch.bfloat16)
             wr = router_weight(E, H, seed * 1000 + i).to(self.device)
-            self.layers.append(GpuMoE(shape, wr, w13, w2))
+            self.layers.append(GpuMoE(shape, wr, w13, w2, workspace=self.workspace))
 
     def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor) -> torch.Tensor:
         """h <- h + MoE_l(RMSNorm(h)) for l in [l0, l1) (Qwen3's pre-MoE norm keeps the

@@ -58,6 +58,24 @@ def _check_tensor(name: str, t: torch.Tensor, shape: tuple, dtype: torch.dtype) 
     require(t.is_contiguous(), f"{name} must be contiguous")
 
 
+class Workspace:
+    """Grow-only device scratch for `lp_moe_*` calls, shareable by every layer that
+    runs on one stream (the library's workspace is per-call scratch whose fixed
+    header every call leaves zeroed, lpmoe.h). A stack of 48 layers then holds one
+    workspace sized for its largest batch instead of 48."""
+
+    def __init__(self, device: torch.device):
+        self.device = torch.device(device)
+        self.buf: torch.Tensor | None = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None  # release first: the caching allocator reuses it stream-ordered
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
 class GpuMoE:
     """One Qwen3-MoE-style sparse MoE block (router + E SwiGLU experts) on sm_100a.
 
@@ -65,7 +83,8 @@ class GpuMoE:
     wr [E,H], w13 [E,2I,H] (gate rows then up rows), w2 [E,H,I], all bf16.
     """
 
-    def __init__(self, shape: MoEShape, wr: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor):
+    def __init__(self, shape: MoEShape, wr: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor,
+                 workspace: Workspace | None = None):
         self.shape = shape
         H, I, E = shape.hidden, shape.ffn, shape.num_experts
         _check_tensor("wr", wr, (E, H), torch.bfloat16)
@@ -74,8 +93,9 @@ class GpuMoE:
         self.wr, self.w13, self.w2 = wr, w13, w2
         self.device = wr.device
         self._lib = _native.load()
-        self._ws: torch.Tensor | None = None
-        self._route_bufs: dict[int, tuple[torch.Tensor, torch.Tensor, torch.Tensor]] = {}
+        self._ws = workspace if workspace is not None else Workspace(self.device)
+        self._route_cap = 0
+        self._route_bufs: tuple[torch.Tensor, torch.Tensor, torch.Tensor] | None = None
 
     # ------------------------------------------------------------ workspace
     def workspace_bytes(self, T: int) -> int:
@@ -83,21 +103,20 @@ class GpuMoE:
         return int(self._lib.lp_moe_workspace_bytes(T, s.hidden, s.ffn, s.num_experts, s.top_k))
 
     def workspace(self, T: int) -> torch.Tensor:
-        need = max(self.workspace_bytes(T), 256)
-        if self._ws is None or self._ws.numel() < need:
-            # zero-filled once: the header holds self-resetting split-K tickets (lpmoe.h)
-            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
-        return self._ws
+        # zero-filled on (re)allocation: the header holds self-resetting scheduler words (lpmoe.h)
+        return self._ws.get(self.workspace_bytes(T))
 
     def _bufs(self, T: int):
-        b = self._route_bufs.get(T)
-        if b is None:
-            k, E = self.shape.top_k, self.shape.num_experts
-            b = (torch.empty((T, k), dtype=torch.int32, device=self.device),
-                 torch.empty((T, k), dtype=torch.float32, device=self.device),
-                 torch.empty((E,), dtype=torch.int32, device=self.device))
-            self._route_bufs[T] = b
-        return b
+        """ids [T,k], w [T,k], counts [E]: views of grow-only buffers (valid until the next call)."""
+        k, E = self.shape.top_k, self.shape.num_experts
+        if self._route_bufs is None or T > self._route_cap:
+            cap = max(T, 2 * self._route_cap)
+            self._route_bufs = (torch.empty((cap, k), dtype=torch.int32, device=self.device),
+                                torch.empty((cap, k), dtype=torch.float32, device=self.device),
+                                torch.empty((E,), dtype=torch.int32, device=self.device))
+            self._route_cap = cap
+        ids, w, counts = self._route_bufs
+        return ids[:T], w[:T], counts
 
     # ------------------------------------------------------------ full layer
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,

@@ -216,3 +216,22 @@ def test_host_pipeline_matches_device_forward(cuda):
         ref, _ = layer(x.to(cuda))
         torch.cuda.synchronize()
         assert torch.equal(y, ref.cpu())
+
+
+@pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1"])
+def test_experimental_paths_match_oracle(cuda, knob):
+    """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, '.'); import torch; "
+        "from tests.test_gpu_moe import check_layer; from paper_2510_08055_b200 import QWEN3_30B_A3B; "
+        "d = torch.device('cuda', 0); "
+        "[check_layer(QWEN3_30B_A3B, T, 5, d) for T in (1, 576, 4100)]; print('ok')"
+    )
+    k, v = knob.split("=")
+    env = dict(os.environ, **{k: v})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

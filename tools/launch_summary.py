@@ -24,8 +24,10 @@ for k, m in data.items():
     t = m["gpu__time_duration.sum"][-4:]
     mean = sum(t) / len(t)
     tot += mean
-    rd = m["dram__bytes_read.sum"][-4:]
-    wr = m["dram__bytes_write.sum"][-4:]
-    out.append((k, mean / 1e3, sum(rd) / len(rd) / 1e6, sum(wr) / len(wr) / 1e6))
-for k, t, r, w in out:
-    print(f"{k:50s} {t:9.2f} us  {100 * t * 1e3 / tot:5.1f}%  read {r:9.1f} MB  write {w:8.1f} MB")
+    rd = m.get("dram__bytes_read.sum", [])[-4:]
+    wr = m.get("dram__bytes_write.sum", [])[-4:]
+    n = len(m["gpu__time_duration.sum"])
+    out.append((k, mean / 1e3, n, sum(rd) / len(rd) / 1e6 if rd else None, sum(wr) / len(wr) / 1e6 if wr else None))
+for k, t, n, r, w in out:
+    extra = f"  read {r:9.1f} MB  write {w:8.1f} MB" if r is not None else ""
+    print(f"{k:50s} {n:5d} launches {t:9.2f} us  {100 * t * 1e3 / tot:5.1f}%{extra}")

@@ -24,7 +24,8 @@ NAMES = {0: "router blk0 start", 1: "router blk0 setup done", 2: "router blk0 fi
          6: "router blk0 end", 8: "router first CTA start", 9: "router last CTA end",
          16: "scan start", 17: "scan staged", 18: "scan end (staged)",
          24: "scatter first", 25: "scatter last", 10: "router blk0 post-mma sync", 11: "router blk0 cluster sync1",
-         12: "router blk0 cluster sync2", 13: "router blk0 top-k done(2)", 14: "router blk0 hist done", 32: "experts first CTA start", 33: "experts blk0 start",
+         12: "router blk0 cluster sync2", 13: "router blk0 top-k done(2)", 14: "router blk0 hist done",
+         15: "router blk0 grid barrier passed", 32: "experts first CTA start", 33: "experts blk0 start",
          34: "experts last CTA end", 35: "experts blk0 end", 40: "combine first", 41: "combine last"}
 
 
