@@ -133,6 +133,18 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(T: int):
+    """DRAM bytes per k_experts launch at this T from the latest committed `ncu --set full`
+    capture (profiles/rNN/k_experts_traffic.json, written by tools/summarize_evidence.py)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k_experts_traffic.json")), reverse=True):
+        d = json.load(open(path)).get(f"k_experts_{T}")
+        if d:
+            return d["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+    return None, None
+
+
 # ----------------------------------------------------------------------------- CPU legs
 def cpu_layer_inputs(T: int, seed: int = 0):
     from paper_2510_08055_b200 import QWEN3_30B_A3B as s
@@ -366,12 +378,15 @@ def run_ours(args, rank: int, world: int):
         nnz = statistics.mean(hits)
         algo_bytes = nnz * s.bytes_per_expert + 2 * T * s.hidden * 2
         achieved = algo_bytes / (stage_us["experts"] * 1e-6) / 1e9
+        traffic, traffic_src = ncu_traffic(T)
+        if traffic_src:
+            traffic_src += " (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         layer_bytes = nnz * s.bytes_per_expert + s.num_experts * s.hidden * 2 + 2 * T * s.hidden * 2 + T * s.top_k * 8
         out["roofline"] = {"bound": "hbm", "kernel": "k_experts (grouped gate/up+SiLU*mul and down, tcgen05); "
                                                      "duration from CUDA events around its launch in a second pass "
                                                      "over the same K steps",
                            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                           "traffic": None, "peak_source": peak_src,
+                           "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                            "algo_bytes_per_launch": algo_bytes,
                            "layer_frac": (layer_bytes / (ms * 1e-3)) / 1e9 / peak}
         out["stages_us"] = stage_us

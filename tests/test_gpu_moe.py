@@ -225,8 +225,8 @@ def test_experimental_paths_match_oracle(cuda, knob):
     import sys
 
     code = (
-        "import sys; sys.path.insert(0, '.'); import torch; "
-        "from tests.test_gpu_moe import check_layer; from paper_2510_08055_b200 import QWEN3_30B_A3B; "
+        "import sys; sys.path[:0] = ['.', 'tests']; import torch; "
+        "from test_gpu_moe import check_layer; from paper_2510_08055_b200 import QWEN3_30B_A3B; "
         "d = torch.device('cuda', 0); "
         "[check_layer(QWEN3_30B_A3B, T, 5, d) for T in (1, 576, 4100)]; print('ok')"
     )
