@@ -52,6 +52,7 @@ struct ExpertsParams {
   __nv_bfloat16* y_perm;       // [S, H]
   uint32_t* sched;             // [0] work counter, [1+e] UP items done for expert e
   int prefetch_kblocks;        // k-blocks of the first item's W13 rows to warm in L2 before pdl_wait
+  int warm_rows;               // W13 rows [0, warm_rows) already warmed in L2 by the router
   int lookahead;               // L2 prefetch distance (k-blocks) for weight tiles ahead of the smem ring; 0 = off
   int weights_evict_first;     // weights loaded with L2::evict_first (1) or evict_normal (0)
   // Fused combine (y != nullptr): DN items count, per (token, 256-feature
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     // assuming one token tile per expert — exact in the memory-bound regime.
     const int mt_up0 = p.I / kTileM;
     const int e_guess = blockIdx.x / mt_up0;
-    if (e_guess < E) {
+    if (e_guess < E && e_guess * 2 * p.I + 2 * p.I > p.warm_rows) {
       const int row = e_guess * 2 * p.I + (blockIdx.x % mt_up0) * kTileM;
       const int kb_pf = min(p.prefetch_kblocks, p.H / kTileK);
       for (int kb = 0; kb < kb_pf; ++kb) {

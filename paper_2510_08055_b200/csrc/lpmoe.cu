@@ -314,7 +314,8 @@ bool fused_route_ok(const Layout& L, int T, int E) {
 }
 
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
-                 void* ws, const Layout& L, cudaStream_t st, const FusedPermute* fp = nullptr) {
+                 void* ws, const Layout& L, cudaStream_t st, const FusedPermute* fp = nullptr,
+                 const void* warm = nullptr, size_t warm_bytes = 0) {
   int rc;
   if ((rc = get_encode())) return rc;
   const int TN = L.chunk_tokens;
@@ -326,6 +327,8 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
   rp.ntiles = ntiles;
+  rp.warm = static_cast<const uint8_t*>(warm);
+  rp.warm_bytes = warm ? warm_bytes : 0;
   const int e_pad = (E + 31) / 32 * 32;
   if (fp) {
     rp.max_n = fp->max_n;
@@ -395,6 +398,17 @@ int prefetch_kblocks() {
   return v;
 }
 
+// Bytes of W13 (from its start, i.e. the first UP items in claim order) the
+// router warms in L2 for the expert kernel. Knob LPMOE_L2_WARM_MB; default 0:
+// measured on B200, the router grid only completes once its bulk prefetches
+// have landed, so the warm-up lengthens the routing critical path as much as
+// it shortens the expert stream (T=576: 224.7 us at 0 MB vs 227.5 at 80 MB).
+size_t l2_warm_bytes(size_t w13_bytes) {
+  static const long mb = env_int("LPMOE_L2_WARM_MB", 0);
+  const size_t b = mb > 0 ? static_cast<size_t>(mb) << 20 : 0;
+  return (b < w13_bytes ? b : w13_bytes) & ~size_t(15);
+}
+
 bool use_gather(int T) {
   static const int v = env_int("LPMOE_GATHER", 0);  // 0 off, 1 on, >1: on from T >= v
   return v == 1 || (v > 1 && T >= v);
@@ -428,10 +442,10 @@ bool use_fused_combine() {
 int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, const void* w13, const void* w2,
                    int H, int I, int E, int max_n, const int32_t* offsets, const int32_t* tile_prefix,
                    const int32_t* tile_rows, uint32_t* sched, void* act, void* y_perm, cudaStream_t st,
-                   const FusedCombine& fc = FusedCombine{}) {
+                   const FusedCombine& fc = FusedCombine{}, int warm_rows = 0) {
   lp::ExpertsParams p{H,       I,           E,        tok_of, offsets, tile_prefix, tile_rows,
                       static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                      prefetch_kblocks(), env_lookahead(), env_wpol(), static_cast<__nv_bfloat16*>(fc.y),
+                      prefetch_kblocks(), warm_rows, env_lookahead(), env_wpol(), static_cast<__nv_bfloat16*>(fc.y),
                       fc.slot_tok, fc.slot_of, fc.wgt, fc.blk_cnt, fc.topk};
   if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
     switch (max_n) {
@@ -602,15 +616,16 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   const bool gather = use_gather(T);
   const bool fused = use_fused_combine();
   const bool fused_route = !fused && fused_route_ok(L, T, E);
+  const size_t warm = l2_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);
   prof_mark(0, st);
   if (fused_route) {  // router + grid barrier + permutation in one launch
     const FusedPermute fp{counts, offsets, slot_of, tok_of, gather ? nullptr : at<void>(ws, L.x_perm), max_n,
                           at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched),
                           at<uint32_t>(ws, kGbarOff)};
-    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, &fp))) return rc;
+    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, &fp, w13, warm))) return rc;
     prof_mark(1, st);
   } else {
-    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st))) return rc;
+    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, nullptr, w13, warm))) return rc;
     prof_mark(1, st);
     if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
                                   gather ? nullptr : at<void>(ws, L.x_perm),
@@ -627,7 +642,7 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
                            w2, H, I, E, max_n, offsets,
                            at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),
-                           at<void>(ws, L.y_perm), st, fc)))
+                           at<void>(ws, L.y_perm), st, fc, static_cast<int>(warm / (static_cast<size_t>(H) * 2)))))
     return rc;
   prof_mark(3, st);
   if (!fused && (rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;

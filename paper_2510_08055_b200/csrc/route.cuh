@@ -53,6 +53,9 @@ struct RouterParams {
   int32_t* tile_rows;     // [E]
   uint32_t* sched;        // [E+1] expert scheduler words, reset here
   uint32_t* gbar;         // [2] grid barrier (arrive, depart); zero on entry, left zero
+  // ---- L2 warm-up of the expert kernel's first weights (forward path only) ----
+  const uint8_t* warm;    // start of the W13 range the expert kernel streams first
+  size_t warm_bytes;      // bytes to prefetch into L2, split across the router grid
 };
 
 // Grid-wide barrier for a co-resident grid (<= 1 CTA per SM, checked by the
@@ -264,6 +267,17 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (threadIdx.x == 64) LP_TRACE_AT(tr, 4);
+    if (threadIdx.x == 64 && p.warm_bytes) {
+      // This CTA's HBM reads are done. The expert kernel streams every touched
+      // expert's weights right after routing: pull its first items' W13 rows
+      // into L2 while the rest of the routing prologue leaves HBM idle.
+      const size_t per = ((p.warm_bytes + gridDim.x - 1) / gridDim.x + 65535) & ~size_t(65535);
+      const size_t lo = per * blockIdx.x, hi = min(p.warm_bytes, lo + per);
+      for (size_t o = lo; o < hi; o += 65536) {
+        const size_t n = hi - o < 65536 ? hi - o : 65536;
+        bulk_prefetch_l2(p.warm + o, static_cast<uint32_t>(n));
+      }
+    }
     for (int mt = 0; mt < p.mtiles; ++mt) {
       const int e = mt * 128 + 32 * q + lane;
       for (int c = 0; c < TN / 16; ++c) {
