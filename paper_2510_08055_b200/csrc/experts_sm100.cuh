@@ -33,7 +33,8 @@
 
 namespace lp {
 
-constexpr int kExpertsThreads = 384;  // w0 TMA+sched, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
+constexpr int kExpertsThreads = 384;  // w0 TMA+sched, w1 MMA, w2 TMEM alloc (+w3: gather), w4..w11 epilogue
+constexpr int kGatherThreads = 64;    // warps 2-3 in GATHER mode
 constexpr int kEpiThreads = 256;
 constexpr int kTileM = 128;        // weight rows per tile
 constexpr int kTileK = 64;         // bf16 elements per 128-byte swizzle row
@@ -66,6 +67,7 @@ struct ExpertsParams {
   const float* wgt;            // [T*topk] routing weights
   uint32_t* blk_cnt;           // [T * ceil(H/256)] completion counters
   int topk;
+  const __nv_bfloat16* xsrc;   // GATHER: [rows, H] token rows read through tok_of by the gather warps
 };
 
 // DN-item tail of the fused combine (256 epilogue threads, named barrier 1).
@@ -147,7 +149,7 @@ struct ExpertsCfg {
   static constexpr int kAccCols = 2 * MAX_N;  // gate | up
   static constexpr int kTmemCols = kAccStages * kAccCols < 32 ? 32 : kAccStages * kAccCols;
   // barriers + ring + scalars + expert tables
-  static constexpr int kAuxBytes = 8 * (2 * kStages + 2 * kAccStages + 2 * kRing) + 16 * kRing + 16 +
+  static constexpr int kAuxBytes = 8 * (3 * kStages + 1 + 2 * kAccStages + 2 * kRing) + 16 * kRing + 16 +
                                    4 * (3 * kMaxExperts + 2) + 4 * MAX_N + 4 * (kEpiThreads + 4);
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
 };
@@ -166,9 +168,11 @@ __device__ __forceinline__ float silu_mul(float g, float u) {
   return fmaf(hg, tanh_approx(hg), hg) * u;
 }
 
-// GATHER: UP items read token rows of an unpermuted [rows, H] source through
-// TMA tile::gather4 (tok_of indices); otherwise rows are expert-contiguous
-// (x_perm) and arrive in 32-row TMA boxes.
+// GATHER: UP items read token rows of the unpermuted [rows, H] source (x)
+// through tok_of: warps 2-3 copy them with 16-byte cp.async straight into the
+// SWIZZLE_128B layout TMA would have produced and arrive on bfull[stage] when
+// their copies land (no x_perm round trip through HBM). Otherwise rows are
+// expert-contiguous (x_perm) and arrive in 32-row TMA boxes.
 template <int MAX_N, bool GATHER>
 __global__ void __launch_bounds__(kExpertsThreads, 1)
     k_experts(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
@@ -186,7 +190,8 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   uint64_t* tempty = tfull + A_;
   uint64_t* sfull = tempty + A_;
   uint64_t* sempty = sfull + kRing;
-  int4* ring = reinterpret_cast<int4*>(sempty + kRing);
+  uint64_t* bfull = sempty + kRing;  // GATHER: B operand (token rows) of the stage landed
+  int4* ring = reinterpret_cast<int4*>(bfull + ((S_ + 1) & ~1));  // 16-byte aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   int32_t* s_off = reinterpret_cast<int32_t*>(tmem_slot + 4);
   int32_t* s_tp = s_off + (kMaxExperts + 1);
@@ -202,7 +207,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiThreads); }
-    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], 2); }
+    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], GATHER ? 4 : 2); }
+    if (GATHER)
+      for (int s = 0; s < S_; ++s) mbar_init(&bfull[s], kGatherThreads);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -294,13 +301,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
       const int nmma = (nvalid + 15) & ~15;
       const bool up = kind == kItemUp;
-      if (GATHER && up) {  // source rows of this item's token tile (pad rows repeat the last valid one)
-        for (int q = lane; q < nmma; q += 32) {
-          const int slot = row0 + min(q, nvalid - 1);
-          s_tok[q] = p.tok_of ? __ldcg(p.tok_of + slot) : slot;
-        }
-      }
-      __syncwarp();
+      (void)nmma;
       if (lane == 0) {
         const int nbox = (nvalid + kBoxRows - 1) / kBoxRows;
         if (!up) {
@@ -309,8 +310,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         }
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
         const bool two = up || m0 + kTileM < p.H;  // second A tile (up rows / upper W2 rows)
-        const uint32_t bytes = (two ? 2 : 1) * kATileBytes +
-                               (GATHER && up ? nmma * 128 : nbox * kBoxRows * 128);
+        const uint32_t bytes = (two ? 2 : 1) * kATileBytes + (GATHER && up ? 0 : nbox * kBoxRows * 128);
         const int arow = up ? e * 2 * p.I + m0 : e * p.H + m0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -330,11 +330,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           if (up) {
             tma_load_2d(sa, &tm_w13, &full[stage], kb * kTileK, arow, pol_w);
             tma_load_2d(sa + kATileBytes, &tm_w13, &full[stage], kb * kTileK, arow + p.I, pol_w);
-            if (GATHER) {
-              for (int g = 0; g < nmma; g += 4)
-                tma_gather4(sb + g * 128, &tm_xsrc, &full[stage], kb * kTileK, s_tok[g], s_tok[g + 1],
-                            s_tok[g + 2], s_tok[g + 3], pol_a);
-            } else {
+            if (!GATHER) {
               for (int b = 0; b < nbox; ++b)
                 tma_load_2d(sb + b * kBoxRows * 128, &tm_xsrc, &full[stage], kb * kTileK, row0 + b * kBoxRows,
                             pol_a);
@@ -374,6 +370,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const uint32_t d_up = d_gate + MAX_N;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (GATHER) mbar_wait(&bfull[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
           const uint64_t a0 = sdesc_kmajor_sw128(sa);
@@ -393,6 +390,52 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       }
     }
     __syncwarp();
+  } else if (GATHER && (warp == 2 || warp == 3)) {
+    // ===================== token-row gather (64 threads, LSU cp.async) =====================
+    // Thread (g, j) copies 16-byte chunk j of rows g, g+8, ... of the item's
+    // token tile; SWIZZLE_128B puts chunk j of row r at chunk slot j ^ (r & 7),
+    // and r & 7 == g for all of this thread's rows.
+    constexpr int RPT = MAX_N / 8;
+    const int gt = threadIdx.x - 64;
+    const int g = gt >> 3, j = gt & 7;
+    const uint64_t pol_x = policy_evict_last();  // x is re-read by every m-tile of the token tile
+    int stage = 0; uint32_t phase = 0;
+    int r = 0; uint32_t rph = 0;
+    while (true) {
+      mbar_wait(&sfull[r], rph);
+      const int4 info = ring[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[r]);
+      if (++r == kRing) { r = 0; rph ^= 1; }
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      if (kind == kItemUp) {
+        const int row0 = info.z, nvalid = info.w;
+        int tok[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int rr = g + 8 * i;
+          tok[i] = rr < nvalid ? __ldg(p.tok_of + row0 + rr) : -1;
+        }
+        const __nv_bfloat16* xs = p.xsrc + j * 8;
+        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
+        for (int kb = 0; kb < p.H / kTileK; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + 2 * kATileBytes) + sw;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+            if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
+          cp_async_arrive_noinc(&bfull[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      } else {  // DN items: B (act rows) comes by TMA; keep bfull's phases in step
+        for (int kb = 0; kb < p.I / kTileK; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive(&bfull[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs -> global =====================
     const int q = warp & 3;                 // TMEM lane quarter this warp may access

@@ -365,6 +365,12 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
   }
   LP_CUDA(launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts, offsets,
                      tile_prefix, tile_rows, sched, zero_buf, zero_n));
+  if (x_perm == nullptr) {
+    LP_CUDA(launch_pdl(lp::k_slots, (S + 255) / 256, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist),
+                       rank_local, static_cast<const int32_t*>(offsets), S, E, topk, chunk_tokens * topk, slot_of,
+                       tok_of));
+    return LP_OK;
+  }
   LP_CUDA(launch_pdl(lp::k_scatter, (S + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
                      static_cast<const int32_t*>(offsets), static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
                      chunk_tokens * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
@@ -409,9 +415,14 @@ size_t l2_warm_bytes(size_t w13_bytes) {
   return (b < w13_bytes ? b : w13_bytes) & ~size_t(15);
 }
 
-bool use_gather(int T) {
-  static const int v = env_int("LPMOE_GATHER", 0);  // 0 off, 1 on, >1: on from T >= v
-  return v == 1 || (v > 1 && T >= v);
+// Token rows reach the expert kernel gathered straight from x by its cp.async
+// warps (no x_perm round trip) in the memory-bound regime (max_n == 64);
+// at larger tiles the per-SM LSU in-flight limit makes the gather slower than
+// TMA boxes from a materialised x_perm (B200, T=2048: 333 vs 321 us; T=8224:
+// 858 vs 824 us; T=576: 212 vs 221 us). LPMOE_GATHER=0/1 forces it off/on.
+bool use_gather(int max_n) {
+  static const int v = env_int("LPMOE_GATHER", -1);
+  return v < 0 ? max_n == 64 : v != 0;
 }
 int env_lookahead() {
   static const int v = env_int("LPMOE_LOOKAHEAD", 0);
@@ -446,8 +457,9 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
   lp::ExpertsParams p{H,       I,           E,        tok_of, offsets, tile_prefix, tile_rows,
                       static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
                       prefetch_kblocks(), warm_rows, env_lookahead(), env_wpol(), static_cast<__nv_bfloat16*>(fc.y),
-                      fc.slot_tok, fc.slot_of, fc.wgt, fc.blk_cnt, fc.topk};
-  if (tok_of) {  // rows gathered by TMA gather4 from the unpermuted source (experimental)
+                      fc.slot_tok, fc.slot_of, fc.wgt, fc.blk_cnt, fc.topk, nullptr};
+  if (tok_of) {  // rows gathered by the kernel's cp.async warps from the unpermuted source
+    p.xsrc = static_cast<const __nv_bfloat16*>(src);
     switch (max_n) {
       case 64: return launch_experts_t<64, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
       case 128: return launch_experts_t<128, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
@@ -613,7 +625,7 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
   // Token rows reach the expert kernel either materialised in slot order
   // (x_perm, one scatter pass) or gathered straight from x by TMA (tok_of).
-  const bool gather = use_gather(T);
+  const bool gather = use_gather(max_n);
   const bool fused = use_fused_combine();
   const bool fused_route = !fused && fused_route_ok(L, T, E);
   const size_t warm = l2_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);

@@ -199,6 +199,25 @@ __global__ void __launch_bounds__(256)
   if (lane == 0) LP_TRACE_MAX(25);
 }
 
+// Index-only scatter (token rows are gathered later by the expert kernel):
+// one thread per routing entry.
+__global__ void __launch_bounds__(256)
+    k_slots(const int32_t* __restrict__ ids, const int32_t* __restrict__ chunk_base,
+            const int32_t* __restrict__ rank_local, const int32_t* __restrict__ offsets, int S, int E, int topk,
+            int chunk, int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) LP_TRACE_MIN(24);
+  if (i >= S) return;
+  const int e = __ldcg(ids + i);
+  const int slot = __ldcg(offsets + e) + __ldcg(chunk_base + static_cast<size_t>(i / chunk) * E + e) +
+                   __ldcg(rank_local + i);
+  slot_of[i] = slot;
+  tok_of[slot] = i / topk;
+  if (threadIdx.x == 0) LP_TRACE_MAX(25);
+}
+
 // x_perm[slot] = x[tok_of[slot]] (standalone lp_moe_permute only; the fused
 // forward never materialises x_perm — the expert kernel gathers rows by TMA).
 __global__ void __launch_bounds__(256)

@@ -218,7 +218,7 @@ def test_host_pipeline_matches_device_forward(cuda):
         assert torch.equal(y, ref.cpu())
 
 
-@pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1"])
+@pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
