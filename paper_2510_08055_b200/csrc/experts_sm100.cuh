@@ -228,9 +228,12 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       }
     }
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  // all 512 TMEM columns (MAX_N = 256) are only claimed once the predecessors
+  // completed, so a co-resident predecessor CTA can never starve on allocation
+  if (warp == 2 && C::kTmemCols < 512) tmem_alloc(tmem_slot, C::kTmemCols);
   pdl_trigger();
   pdl_wait();
+  if (warp == 2 && C::kTmemCols >= 512) tmem_alloc(tmem_slot, C::kTmemCols);
   for (int i = threadIdx.x; i <= E; i += blockDim.x) { s_off[i] = p.offsets[i]; s_tp[i] = p.tile_prefix[i]; }
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_ts[i] = p.tile_rows[i];
   tc_fence_before();
@@ -492,6 +495,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       if (++acc == A_) { acc = 0; aph ^= 1; }
       if (kind == kItemUp) fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
       if (kind == kItemDown && p.y != nullptr) fused_combine(p, m0, row0, nvalid, et, s_fin);
+      if (kind == kItemUp) named_bar_sync(1, kEpiThreads);  // every thread's act stores precede the count
       if (et == 0) {
         mbar_arrive(&sempty[r]);
         if (kind == kItemUp) {  // release: every epilogue thread's act stores precede the count

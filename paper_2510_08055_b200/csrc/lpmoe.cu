@@ -15,6 +15,7 @@
 
 #include "../../include/lpmoe.h"
 #include "experts_sm100.cuh"
+#include "experts_pair_sm100.cuh"
 #include "norm.cuh"
 #include "permute.cuh"
 #include "route.cuh"
@@ -394,6 +395,50 @@ int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, c
   return LP_OK;
 }
 
+// Compute-bound regime (max_n == 256): the expert kernel on CTA pairs
+// (cta_group::2, experts_pair_sm100.cuh). LPMOE_PAIR=0 selects k_experts<256>.
+bool use_pair(int max_n, int H, int I) {
+  static const int v = env_int("LPMOE_PAIR", 1);
+  return v != 0 && max_n == 256 && H % 512 == 0 && I % 256 == 0;
+}
+
+int launch_experts_pair(const void* x_perm, int S, const void* act, const void* w13, const void* w2, int H, int I,
+                        int E, const lp::ExpertsParams& p, cudaStream_t st) {
+  int rc;
+  if ((rc = get_encode())) return rc;
+  CUtensorMap tm_w13, tm_w2, tm_x, tm_act;
+  if ((rc = make_tmap(&tm_w13, w13, static_cast<uint64_t>(E) * 2 * I, H, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_x, x_perm, S, H, lp::kBoxRows))) return rc;
+  if ((rc = make_tmap(&tm_act, act, S, I, lp::kBoxRows))) return rc;
+  constexpr int smem = lp::PairCfg::kSmemBytes;
+  if ((rc = set_smem(lp::k_experts_pair, smem))) return rc;
+  const int sms = sm_count();
+  static int max_clusters = -1;  // pairs that fit at once (one CTA per SM)
+  if (max_clusters < 0) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(sms & ~1);
+    cfg.blockDim = dim3(lp::kExpertsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, lp::k_experts_pair, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = sms / 2;
+    }
+    max_clusters = n < sms / 2 ? n : sms / 2;
+  }
+  LP_CUDA(launch_pdl_cluster(lp::k_experts_pair, 2 * max_clusters, lp::kExpertsThreads, smem, st, 2, tm_w13, tm_w2,
+                             tm_x, tm_act, p));
+  return LP_OK;
+}
+
 // k-blocks of the first item's W13 warmed in L2 before pdl_wait (2 x 16 KiB each);
 // tuning knob LPMOE_PREFETCH_KB (default 16 -> 0.5 MiB per CTA).
 int prefetch_kblocks() {
@@ -466,6 +511,7 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
       default: return launch_experts_t<256, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
     }
   }
+  if (fc.y == nullptr && use_pair(max_n, H, I)) return launch_experts_pair(src, S, act, w13, w2, H, I, E, p, st);
   switch (max_n) {
     case 64: return launch_experts_t<64, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
     case 128: return launch_experts_t<128, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);

@@ -218,7 +218,8 @@ def test_host_pipeline_matches_device_forward(cuda):
         assert torch.equal(y, ref.cpu())
 
 
-@pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0"])
+@pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
+                                  "LPMOE_PAIR=0"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
@@ -234,4 +235,29 @@ def test_experimental_paths_match_oracle(cuda, knob):
     env = dict(os.environ, **{k: v})
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_back_to_back_layers_large_T(cuda):
+    """Consecutive layers without host sync (PDL chains across layers) at the compute-bound size.
+
+    Regression: the CTA-pair expert kernel once claimed all TMEM before its
+    predecessors finished and deadlocked against them; run in a subprocess
+    under a timeout so a hang fails the test instead of the suite.
+    """
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests']; import torch; "
+        "from test_gpu_moe import make; from paper_2510_08055_b200 import QWEN3_30B_A3B as s; "
+        "from paper_2510_08055_b200.synthetic import router_tokens; "
+        "d = torch.device('cuda', 0); L = [make(s, i, d)[3] for i in range(2)]; "
+        "xs = [router_tokens(8224, s.hidden, 50 + i).to(d) for i in range(4)]; "
+        "ys = [L[i % 2](xs[i % 4])[0] for i in range(24)]; torch.cuda.synchronize(); "
+        "ref = L[23 % 2](xs[23 % 4])[0]; torch.cuda.synchronize(); "
+        "assert torch.equal(ys[23], ref); print('ok')"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
