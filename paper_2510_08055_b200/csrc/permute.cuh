@@ -190,11 +190,19 @@ __global__ void __launch_bounds__(256)
     slot_of[i] = slot;
     tok_of[slot] = t;
   }
-  if (x_perm != nullptr) {
+  if (x_perm != nullptr) {  // all of the lane's loads in flight, then the stores
     const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
     uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
     const int nv = H / 8;
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+    int v = lane;
+    for (; v + 7 * 32 < nv; v += 8 * 32) {
+      uint4 d[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] = __ldg(src + v + u * 32);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dst[v + u * 32] = d[u];
+    }
+    for (; v < nv; v += 32) dst[v] = __ldg(src + v);
   }
   if (lane == 0) LP_TRACE_MAX(25);
 }
@@ -260,6 +268,23 @@ __global__ void __launch_bounds__(kCombineThreads)
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.f;
     int j = 0;
+    for (; j + 8 <= topk; j += 8) {  // eight rows in flight
+      uint4 d[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        d[u] = __ldcs(reinterpret_cast<const uint4*>(y_perm + static_cast<size_t>(s_slot[j + u]) * H) + v);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d[u]);
+        const float wj = s_w[j + u];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(h2[q]);
+          acc[2 * q] += wj * f.x;
+          acc[2 * q + 1] += wj * f.y;
+        }
+      }
+    }
     for (; j + 4 <= topk; j += 4) {
       uint4 d[4];
 #pragma unroll

@@ -67,7 +67,7 @@ def main():
     with open(os.path.join(dst, "k_experts_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     for fn in ("bench.jsonl", "bench_ref.jsonl", "bench_sweep.jsonl", "serving_c3.jsonl", "serving_c4.jsonl",
-               "serving_c5.jsonl", "pytest_gpu.log", "smoke.log"):
+               "serving_c5.jsonl", "pytest_gpu.log", "smoke.log", "trace_T576.txt", "k_experts_576.ncu-rep"):
         p = os.path.join(ev, fn)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(dst, fn))
