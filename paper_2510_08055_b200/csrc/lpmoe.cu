@@ -519,39 +519,6 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
   }
 }
 
-// L2 warm-up of the first bytes of W13 (the expert kernel's first UP items in
-// claim order) on a side stream while the routing prologue runs on the main
-// stream: HBM is otherwise idle until the expert kernel starts streaming.
-__global__ void k_l2_warm(const uint8_t* __restrict__ p, size_t bytes) {
-  const size_t per = ((bytes + gridDim.x - 1) / gridDim.x + 65535) & ~size_t(65535);
-  const size_t lo = per * blockIdx.x;
-  const size_t hi = lo + per < bytes ? lo + per : bytes;
-  if (threadIdx.x == 0)
-    for (size_t o = lo; o < hi; o += 65536) lp::bulk_prefetch_l2(p + o, static_cast<uint32_t>(hi - o < 65536 ? hi - o : 65536));
-}
-
-struct SideStream {
-  cudaStream_t st = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  bool ok = false;
-  SideStream() {
-    ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
-         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
-  }
-};
-thread_local SideStream* g_side = nullptr;
-
-size_t side_warm_bytes(size_t w13_bytes) {
-  static const long mb = env_int("LPMOE_SIDE_WARM_MB", 0);
-  const size_t b = mb > 0 ? static_cast<size_t>(mb) << 20 : 0;
-  return (b < w13_bytes ? b : w13_bytes) & ~size_t(15);
-}
-int side_join_at_end() {
-  static const int v = env_int("LPMOE_SIDE_JOIN", 0);
-  return v;
-}
-
 // Tile schedule from externally supplied offsets (staged / expert-parallel use).
 __global__ void k_plan(const int32_t* __restrict__ offsets, int E, int max_n, int32_t* __restrict__ tile_prefix,
                        int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched) {
@@ -708,16 +675,6 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   const bool fused = use_fused_combine();
   const bool fused_route = !fused && fused_route_ok(L, T, E);
   const size_t warm = l2_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);
-  const size_t side_warm = side_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);
-  if (side_warm) {
-    if (!g_side) g_side = new SideStream();
-    if (!g_side->ok) return fail(LP_ECUDA, "side stream creation failed");
-    LP_CUDA(cudaEventRecord(g_side->fork, st));
-    LP_CUDA(cudaStreamWaitEvent(g_side->st, g_side->fork, 0));
-    k_l2_warm<<<32, 32, 0, g_side->st>>>(static_cast<const uint8_t*>(w13), side_warm);
-    LP_CHECK_LAUNCH("k_l2_warm");
-    LP_CUDA(cudaEventRecord(g_side->join, g_side->st));
-  }
   prof_mark(0, st);
   if (fused_route) {  // router + grid barrier + permutation in one launch
     const FusedPermute fp{counts, offsets, slot_of, tok_of, gather ? nullptr : at<void>(ws, L.x_perm), max_n,
@@ -746,10 +703,8 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
                            at<void>(ws, L.y_perm), st, fc, static_cast<int>(warm / (static_cast<size_t>(H) * 2)))))
     return rc;
   prof_mark(3, st);
-  if (side_warm && !side_join_at_end()) LP_CUDA(cudaStreamWaitEvent(st, g_side->join, 0));
   if (!fused && (rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;
   prof_mark(4, st);
-  if (side_warm && side_join_at_end()) LP_CUDA(cudaStreamWaitEvent(st, g_side->join, 0));
   return ok();
 }
 

@@ -190,19 +190,11 @@ __global__ void __launch_bounds__(256)
     slot_of[i] = slot;
     tok_of[slot] = t;
   }
-  if (x_perm != nullptr) {  // all of the lane's loads in flight, then the stores
+  if (x_perm != nullptr) {
     const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
     uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
     const int nv = H / 8;
-    int v = lane;
-    for (; v + 7 * 32 < nv; v += 8 * 32) {
-      uint4 d[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) d[u] = __ldg(src + v + u * 32);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) dst[v + u * 32] = d[u];
-    }
-    for (; v < nv; v += 32) dst[v] = __ldg(src + v);
+    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
   }
   if (lane == 0) LP_TRACE_MAX(25);
 }
