@@ -57,12 +57,17 @@ struct PairCfg {
   static constexpr int kStageBytes = 2 * kATileBytes + kBRows * 128;
   static constexpr int kStages = 4;
   static constexpr int kTmemCols = 2 * kN;            // gate | up (single-buffered)
-  static constexpr int kAuxBytes = 8 * (2 * kStages + 2 + 2 * kRing) + 16 * kRing + 16 + 4 * (3 * kMaxExperts + 2);
+  static constexpr int kAuxBytes = 8 * (3 * kStages + 2 + 2 * kRing) + 16 * kRing + 16 + 4 * (3 * kMaxExperts + 2);
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
   static constexpr int kUpFeat = 128;                 // act features per CTA per UP item
   static constexpr int kDnRows = 256;                 // W2 rows per CTA per DN item
 };
 
+// GATHER: UP items' token rows come straight from x (tok_of) through 16-byte
+// cp.async by warps 2-3 of each CTA (its half of the tile), as in k_experts'
+// memory-bound path; the peer's completions are relayed to the leader's B-full
+// barrier by the peer's otherwise idle warp 1. No x_perm is materialised.
+template <bool GATHER>
 __global__ void __launch_bounds__(kExpertsThreads, 1)
     k_experts_pair(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_act,
@@ -78,7 +83,8 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   uint64_t* tempty = tfull + 1;                       // leader's counts both CTAs' epilogue warps
   uint64_t* sfull = tempty + 1;
   uint64_t* sempty = sfull + kRing;                   // leader's counts both CTAs' consumers
-  int4* ring = reinterpret_cast<int4*>(sempty + kRing);
+  uint64_t* bfull = sempty + kRing;                   // GATHER: this CTA's B half landed (+ peer relay on the leader)
+  int4* ring = reinterpret_cast<int4*>(bfull + S_);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   int32_t* s_off = reinterpret_cast<int32_t*>(tmem_slot + 4);
   int32_t* s_tp = s_off + (kMaxExperts + 1);
@@ -94,7 +100,11 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, 16);  // 8 epilogue warps x 2 CTAs
-    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], 4); }
+    // ring consumers: MMA + epilogue (leader), producer + epilogue (peer); GATHER adds
+    // both CTAs' two gather warps and the peer's relay
+    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], GATHER ? 9 : 4); }
+    if (GATHER)
+      for (int s = 0; s < S_; ++s) mbar_init(&bfull[s], kGatherThreads + (leader ? 1 : 0));
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -191,7 +201,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           fence_proxy_async_global();
         }
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
-        const uint32_t bytes = 2 * (2 * kATileBytes + nbox * kBoxRows * 128);
+        const uint32_t bytes = 2 * (2 * kATileBytes + (GATHER && up ? 0 : nbox * kBoxRows * 128));
         const int f = m0 + static_cast<int>(rank) * (up ? C::kUpFeat : C::kDnRows);
         const int arow = up ? e * 2 * p.I + f : e * p.H + f;
         const int arow2 = up ? arow + p.I : arow + kTileM;
@@ -204,8 +214,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_2d_pair(sa, ta, &full[stage], kb * kTileK, arow, pol_w);
           tma_load_2d_pair(sa + kATileBytes, ta, &full[stage], kb * kTileK, arow2, pol_w);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d_pair(sb + b * kBoxRows * 128, tb, &full[stage], kb * kTileK, brow + b * kBoxRows, pol_a);
+          if (!(GATHER && up))
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d_pair(sb + b * kBoxRows * 128, tb, &full[stage], kb * kTileK, brow + b * kBoxRows, pol_a);
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
       }
@@ -232,6 +243,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const uint32_t d0 = tmem_base, d1 = tmem_base + C::kN;
         for (int kb = 0; kb < kblocks; ++kb) {
           PW_LOCAL(&full[stage], phase, "mma:full");
+          if (GATHER) PW_LOCAL(&bfull[stage], phase, "mma:bfull");
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
           const uint64_t a0 = sdesc_kmajor_sw128(sa);
@@ -249,8 +261,81 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         mma_commit_pair(tfull);
         aph ^= 1;
       }
+    } else if (GATHER && !leader && lane == 0) {
+      // relay: the peer's B half of a stage landed -> arrive on the leader's bfull
+      const uint32_t bfull_leader0 = mapa_shared(smem_u32(&bfull[0]), 0);
+      const uint32_t sempty_leader0 = mapa_shared(smem_u32(&sempty[0]), 0);
+      int stage = 0; uint32_t phase = 0;
+      int r = 0; uint32_t rph = 0;
+      while (true) {
+        PW_CLUSTER(&sfull[r], rph, "relay:sfull");
+        const int4 info = ring[r];
+        mbar_arrive_remote(sempty_leader0 + r * 8);
+        if (++r == kRing) { r = 0; rph ^= 1; }
+        const int kind = info.x & 0xff;
+        if (kind == kItemEnd) break;
+        const int kblocks = kind == kItemUp ? p.H / kTileK : p.I / kTileK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          PW_LOCAL(&bfull[stage], phase, "relay:bfull");
+          mbar_arrive_remote(bfull_leader0 + stage * 8);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      }
     }
     __syncwarp();
+  } else if (GATHER && (warp == 2 || warp == 3)) {
+    // ===================== token-row gather (64 threads per CTA, LSU cp.async) =====================
+    // Thread (g, j) copies 16-byte chunk j of rows g, g+8, ... of this CTA's
+    // half of the token tile into the SWIZZLE_128B layout (chunk slot j ^ g).
+    constexpr int RPT = C::kBRows / 8;
+    const int gt = threadIdx.x - 64;
+    const int g = gt >> 3, j = gt & 7;
+    const uint64_t pol_x = policy_evict_last();
+    const uint32_t sempty_leader0 = mapa_shared(smem_u32(&sempty[0]), 0);
+    int stage = 0; uint32_t phase = 0;
+    int r = 0; uint32_t rph = 0;
+    while (true) {
+      if (leader) PW_LOCAL(&sfull[r], rph, "gather:sfull");
+      else PW_CLUSTER(&sfull[r], rph, "gather:sfull");
+      const int4 info = ring[r];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&sempty[r]);
+        else mbar_arrive_remote(sempty_leader0 + r * 8);
+      }
+      if (++r == kRing) { r = 0; rph ^= 1; }
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      if (kind == kItemUp) {
+        const int row0 = info.z, nvalid = info.w;
+        const int half = ((nvalid + 15) & ~15) / 2;
+        const int base = static_cast<int>(rank) * half;  // first tile row of this CTA's half
+        const int mine = min(half, nvalid - base);         // valid rows in this half (may be <= 0)
+        int tok[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int rr = g + 8 * i;
+          tok[i] = rr < mine ? __ldg(p.tok_of + row0 + base + rr) : -1;
+        }
+        const __nv_bfloat16* xs = p.xsrc + j * 8;
+        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
+        for (int kb = 0; kb < p.H / kTileK; ++kb) {
+          PW_LOCAL(&empty[stage], phase ^ 1, "gather:empty");
+          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + 2 * kATileBytes) + sw;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+            if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
+          cp_async_arrive_noinc(&bfull[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      } else {  // DN items: B comes by TMA; keep bfull's phases in step
+        for (int kb = 0; kb < p.I / kTileK; ++kb) {
+          PW_LOCAL(&empty[stage], phase ^ 1, "gather:empty");
+          mbar_arrive(&bfull[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs -> global =====================
     const int q = warp & 3;             // TMEM lane quarter this warp may access

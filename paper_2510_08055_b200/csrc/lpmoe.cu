@@ -402,17 +402,18 @@ bool use_pair(int max_n, int H, int I) {
   return v != 0 && max_n == 256 && H % 512 == 0 && I % 256 == 0;
 }
 
-int launch_experts_pair(const void* x_perm, int S, const void* act, const void* w13, const void* w2, int H, int I,
-                        int E, const lp::ExpertsParams& p, cudaStream_t st) {
+template <bool GATHER>
+int launch_experts_pair(const void* src, int src_rows, int S, const void* act, const void* w13, const void* w2, int H,
+                        int I, int E, const lp::ExpertsParams& p, cudaStream_t st) {
   int rc;
   if ((rc = get_encode())) return rc;
   CUtensorMap tm_w13, tm_w2, tm_x, tm_act;
   if ((rc = make_tmap(&tm_w13, w13, static_cast<uint64_t>(E) * 2 * I, H, lp::kTileM))) return rc;
   if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
-  if ((rc = make_tmap(&tm_x, x_perm, S, H, lp::kBoxRows))) return rc;
+  if ((rc = make_tmap(&tm_x, src, src_rows, H, lp::kBoxRows))) return rc;
   if ((rc = make_tmap(&tm_act, act, S, I, lp::kBoxRows))) return rc;
   constexpr int smem = lp::PairCfg::kSmemBytes;
-  if ((rc = set_smem(lp::k_experts_pair, smem))) return rc;
+  if ((rc = set_smem(lp::k_experts_pair<GATHER>, smem))) return rc;
   const int sms = sm_count();
   static int max_clusters = -1;  // pairs that fit at once (one CTA per SM)
   if (max_clusters < 0) {
@@ -428,13 +429,13 @@ int launch_experts_pair(const void* x_perm, int S, const void* act, const void* 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, lp::k_experts_pair, &cfg) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&n, lp::k_experts_pair<GATHER>, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = sms / 2;
     }
     max_clusters = n < sms / 2 ? n : sms / 2;
   }
-  LP_CUDA(launch_pdl_cluster(lp::k_experts_pair, 2 * max_clusters, lp::kExpertsThreads, smem, st, 2, tm_w13, tm_w2,
+  LP_CUDA(launch_pdl_cluster(lp::k_experts_pair<GATHER>, 2 * max_clusters, lp::kExpertsThreads, smem, st, 2, tm_w13, tm_w2,
                              tm_x, tm_act, p));
   return LP_OK;
 }
@@ -467,7 +468,8 @@ size_t l2_warm_bytes(size_t w13_bytes) {
 // 858 vs 824 us; T=576: 212 vs 221 us). LPMOE_GATHER=0/1 forces it off/on.
 bool use_gather(int max_n) {
   static const int v = env_int("LPMOE_GATHER", -1);
-  return v < 0 ? max_n == 64 : v != 0;
+  static const int pair_v = env_int("LPMOE_PAIR_GATHER", 0);
+  return v < 0 ? (max_n == 64 || (max_n == 256 && pair_v != 0)) : v != 0;
 }
 int env_lookahead() {
   static const int v = env_int("LPMOE_LOOKAHEAD", 0);
@@ -503,6 +505,13 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
                       static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
                       prefetch_kblocks(), warm_rows, env_lookahead(), env_wpol(), static_cast<__nv_bfloat16*>(fc.y),
                       fc.slot_tok, fc.slot_of, fc.wgt, fc.blk_cnt, fc.topk, nullptr};
+  if (fc.y == nullptr && use_pair(max_n, H, I)) {
+    if (tok_of) {  // rows gathered by the kernel's cp.async warps from the unpermuted source
+      p.xsrc = static_cast<const __nv_bfloat16*>(src);
+      return launch_experts_pair<true>(src, src_rows, S, act, w13, w2, H, I, E, p, st);
+    }
+    return launch_experts_pair<false>(src, S, S, act, w13, w2, H, I, E, p, st);
+  }
   if (tok_of) {  // rows gathered by the kernel's cp.async warps from the unpermuted source
     p.xsrc = static_cast<const __nv_bfloat16*>(src);
     switch (max_n) {
@@ -511,7 +520,6 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
       default: return launch_experts_t<256, true>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
     }
   }
-  if (fc.y == nullptr && use_pair(max_n, H, I)) return launch_experts_pair(src, S, act, w13, w2, H, I, E, p, st);
   switch (max_n) {
     case 64: return launch_experts_t<64, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);
     case 128: return launch_experts_t<128, false>(src, src_rows, act, S, w13, w2, H, I, E, p, st);

@@ -96,6 +96,21 @@ def test_skewed_routing_multi_tile(cuda):
     assert ref["counts"][:8].tolist() == [700] * 8
 
 
+def test_skewed_routing_pair_kernel_tiny_tiles(cuda):
+    """Compute-bound regime (CTA-pair kernel) with multi-tile experts AND experts holding 1-15 tokens
+    (MMA N = 16, i.e. 8 B rows per CTA of the pair)."""
+    s = QWEN3_30B_A3B
+    T = 1600
+    wr = router_weight(s.num_experts, s.hidden, 43).float()
+    wr[:8, s.hidden - 1] = 16.0
+    x = router_tokens(T, s.hidden, 45)
+    x[1::67, s.hidden - 1] = 0.0  # ~24 tokens lose the bias and spread over the other experts
+    err, stats, ref = check_layer(s, T, 43, cuda, x=x, wr_override=wr.to(torch.bfloat16))
+    counts = ref["counts"]
+    assert counts[:8].min() > 256                      # several token tiles per hot expert
+    assert ((counts[8:] > 0) & (counts[8:] < 16)).any()  # cold experts with a tiny tile
+
+
 def test_staged_api_matches_fused(cuda):
     s = QWEN3_30B_A3B
     wr, w13, w2, layer = make(s, 21, cuda)
@@ -219,7 +234,7 @@ def test_host_pipeline_matches_device_forward(cuda):
 
 
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
-                                  "LPMOE_PAIR=0"])
+                                  "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
