@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=T_DECODE + T_PREFILL)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 exchange: fused dispatch/combine over peer memory (ep.PeerEP) or NCCL all_to_all")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -214,7 +216,7 @@ def run_ours(args, rank: int, world: int):
     from paper_2510_08055_b200.moe import GpuMoE
     from paper_2510_08055_b200.synthetic import router_tokens, router_weight
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     clocks = ClockSampler(local).start()
@@ -222,7 +224,7 @@ def run_ours(args, rank: int, world: int):
     lib = _native.load()
 
     if world > 1:
-        from paper_2510_08055_b200.ep import EPMoE
+        from paper_2510_08055_b200.ep import EPMoE, PeerEP
     layers = []
     for i in range(N_LAYER_SETS):
         g = torch.Generator(device=dev).manual_seed(1000 + i)
@@ -230,7 +232,11 @@ def run_ours(args, rank: int, world: int):
         w13 = (torch.randn((s.num_experts, 2 * s.ffn, s.hidden), generator=g, device=dev) * 0.02).to(torch.bfloat16)
         w2 = (torch.randn((s.num_experts, s.hidden, s.ffn), generator=g, device=dev) * 0.02).to(torch.bfloat16)
         if world > 1:
-            layers.append(EPMoE.from_full(s, wr, w13, w2, rank, world))
+            if args.ep == "p2p":  # one symmetric IPC region shared by the layer sets (layers run in sequence)
+                layers.append(PeerEP.from_full(s, wr, w13, w2, rank, world, max_tokens=T,
+                                               share=layers[0] if layers else None))
+            else:
+                layers.append(EPMoE.from_full(s, wr, w13, w2, rank, world))
         else:
             layers.append(GpuMoE(s, wr, w13, w2))
         del g
@@ -297,7 +303,7 @@ def run_ours(args, rank: int, world: int):
     barrier()
     ms = start.elapsed_time(end) / K
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if _shared_gpu() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -343,7 +349,7 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / K
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device="cpu" if _shared_gpu() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
@@ -365,13 +371,18 @@ def run_ours(args, rank: int, world: int):
         "config": {"workload": f"qwen3-30b-a3b MoE layer, T={T} ({T_DECODE} decode + {T - T_DECODE} prefill)",
                    "tokens": T, "hidden": s.hidden, "ffn": s.ffn, "experts": s.num_experts, "top_k": s.top_k,
                    "parallelism": f"ep{world}" if world > 1 else "single",
+                   "ep_exchange": (("peer-memory fused dispatch/combine (CUDA IPC, NVLink P2P)" if args.ep == "p2p"
+                                    else "NCCL all_to_all_single") if world > 1 else None),
                    "l2": f"inputs larger than L2: {N_LAYER_SETS} layer weight sets "
                          f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                 "d2h_bytes_per_step": T * s.hidden * 2},
         # ours per step: fused path = router, scan, scatter, experts, combine; EP adds the
         # standalone permutes (3 each), the expert-plan kernel and a second combine
-        "gpu_launches": (5 if world == 1 else 11) * K,
+        # ours per step: fused layer 5 (router, scan, slots/scatter, experts, combine); NCCL EP 11 (+NCCL's);
+        # peer-memory EP 14 (route, chunk_hist, scan, slots, post_counts, plan, dispatch, k_plan, experts,
+        # combine, 4 barriers)
+        "gpu_launches": (5 if world == 1 else (14 if args.ep == "p2p" else 11)) * K,
         "clocks": clocks.summary(t_region0, t_region1),
     }
     if stage_us is not None:
@@ -391,12 +402,20 @@ def run_ours(args, rank: int, world: int):
                            "layer_frac": (layer_bytes / (ms * 1e-3)) / 1e9 / peak}
         out["stages_us"] = stage_us
         out["experts_hit_mean"] = nnz
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is a rank-0, N=1 measurement
         v, cores, n = time_cpu_oracle(T, args.cpu_seconds)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                "sample": f"median of {n} full T={T} layer forwards of the fp32 numpy oracle "
                                          f"(torch/BLAS threads={cores}); reference moesim has no numerical layer"}
     print(json.dumps(out), flush=True)
+
+
+def _shared_gpu() -> bool:
+    return os.environ.get("LPMOE_BENCH_SHARED_GPU", "0") == "1"
+
+
+def _local_device() -> int:
+    return 0 if _shared_gpu() else int(os.environ.get("LOCAL_RANK", 0))
 
 
 def main():
@@ -410,8 +429,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_local_device())
+        # LPMOE_BENCH_SHARED_GPU=1 (protocol testing only): every rank on cuda:0 over gloo, so the
+        # N>1 path (peer-memory EP over CUDA IPC) runs end to end on a one-GPU box; its timings
+        # are meaningless (the ranks' contexts time-slice one GPU)
+        dist.init_process_group("gloo" if _shared_gpu() else "nccl")
     try:
         run_ours(args, rank, world)
     finally:

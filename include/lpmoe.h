@@ -112,6 +112,53 @@ int lp_add_rmsnorm(void* h, const void* delta, void* xn, int T, int H, float eps
  * stage boundaries route | permute | experts | combine | end. n = 0 clears. */
 int lp_profile_events(void* const* events, int n);
 
+/* ---------------------------------------------------------------------------
+ * Expert parallelism over peer memory (ep.py PeerEP). Replaces the two
+ * all_to_all_single exchanges of the NCCL EP path (ep.py EPMoE.forward) with
+ * the dispatch fused into the permutation and the return fused into the
+ * combine, reading/writing the other ranks' buffers through CUDA IPC mappings
+ * (NVLink/NVSwitch P2P across GPUs). The reference has no multi-GPU code
+ * (SPEC.md:24); the per-layer MoE call it stands for is engine.py:144-154.
+ * `peer_*` arguments are DEVICE arrays of P device pointers (index = rank),
+ * the caller's own buffer included. */
+
+/* CUDA IPC export / import of a device allocation (64-byte opaque handle).
+ * lp_ipc_handle names the allocation containing dptr and returns dptr's byte
+ * offset in it; lp_ipc_open maps a handle from ANOTHER process (peer access
+ * enabled lazily) and returns the allocation base. */
+int lp_ipc_handle(const void* dptr, void* handle64, size_t* offset);
+int lp_ipc_open(const void* handle64, void** dptr);
+int lp_ipc_close(void* dptr);
+
+/* Device-side barrier over P ranks: adds 1 to every rank's uint32 counter
+ * (system-scope release), then waits until peer_flag[rank] reaches `target`
+ * (= P x number of barriers so far, counters only grow). */
+int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, void* stream);
+
+/* inbox_d[rank*El + el] = counts[d*El + el] for every rank d (counts: this
+ * rank's per-global-expert routing counts, int32 [P*El]). */
+int lp_ep_post_counts(const int32_t* counts, int32_t* const* peer_inbox, int P, int El, int rank, void* stream);
+
+/* After the barrier that follows post_counts: dest_base[d*El+el] = first row
+ * of this rank's entries for expert el in rank d's receive buffer (rows
+ * expert-major, source-rank-major within an expert); off_local[0..El] = this
+ * rank's expert offsets over all sources (off_local[El] = rows received). */
+int lp_ep_plan(int32_t* const* peer_inbox, int P, int El, int rank, int32_t* dest_base, int32_t* off_local,
+               void* stream);
+
+/* Fused permute + dispatch: entry i = t*topk + j (ids/slot_of/offsets from
+ * lp_moe_route + lp_moe_permute over the P*El global experts) stores x[t]
+ * into peer_recv[d][dest_base[d*El+el] + slot_of[i] - offsets[e]] (bf16
+ * [cap, H] on every rank); records dest_rank[i], dest_row[i]. */
+int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, const int32_t* offsets,
+                   const int32_t* dest_base, void* const* peer_recv, int T, int H, int topk, int El,
+                   int32_t* dest_rank, int32_t* dest_row, void* stream);
+
+/* Fused receive + combine: y[t] = sum_j w[t,j] * peer_y[dest_rank][dest_row]
+ * (fp32 accumulate in fixed j order, bf16 out) read straight from the owners. */
+int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* dest_row, const float* w, int T,
+                  int H, int topk, void* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

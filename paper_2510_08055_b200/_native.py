@@ -40,6 +40,14 @@ SIGNATURES = {
     "lp_union_counts_weighted": (_i, [_p, _i, _i, _i, _i, _p, _p, _p]),
     "lp_add_rmsnorm": (_i, [_p, _p, _p, _i, _i, ctypes.c_float, _p]),
     "lp_profile_events": (_i, [_p, _i]),
+    "lp_ipc_handle": (_i, [_p, _p, _p]),
+    "lp_ipc_open": (_i, [_p, _p]),
+    "lp_ipc_close": (_i, [_p]),
+    "lp_ep_barrier": (_i, [_p, _i, _i, ctypes.c_uint32, _p]),
+    "lp_ep_post_counts": (_i, [_p, _p, _i, _i, _i, _p]),
+    "lp_ep_plan": (_i, [_p, _i, _i, _i, _p, _p, _p]),
+    "lp_ep_dispatch": (_i, [_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _p, _p, _p]),
+    "lp_ep_combine": (_i, [_p, _p, _p, _p, _i, _i, _i, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -16,6 +16,7 @@
 #include "../../include/lpmoe.h"
 #include "experts_sm100.cuh"
 #include "experts_pair_sm100.cuh"
+#include "ep_p2p.cuh"
 #include "norm.cuh"
 #include "permute.cuh"
 #include "route.cuh"
@@ -762,6 +763,100 @@ int lp_profile_events(void* const* events, int n) {
   if (n < 0 || (n > 0 && !events)) return fail(LP_EINVAL, "lp_profile_events: bad arguments");
   g_prof_n = n >= 5 ? 5 : 0;
   for (int i = 0; i < 5; ++i) g_prof[i] = (g_prof_n && i < n) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+  return ok();
+}
+
+// ---------------------------------------------------------------- expert parallelism over peer memory
+int lp_ipc_handle(const void* dptr, void* handle64, size_t* offset) {
+  if (!dptr || !handle64 || !offset) return fail(LP_EINVAL, "lp_ipc_handle: null pointer argument");
+  // the handle names the whole allocation (e.g. a caching-allocator segment):
+  // report dptr's offset from its base so the importer can rebase
+  static PFN_cuMemGetAddressRange_v3020 range_fn = nullptr;
+  if (!range_fn) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(LP_ECUDA, "cuMemGetAddressRange entry point unavailable");
+    range_fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+    return fail(LP_ECUDA, "cuMemGetAddressRange failed");
+  *offset = reinterpret_cast<CUdeviceptr>(dptr) - base;
+  cudaIpcMemHandle_t h;
+  LP_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  return ok();
+}
+
+int lp_ipc_open(const void* handle64, void** dptr) {
+  if (!handle64 || !dptr) return fail(LP_EINVAL, "lp_ipc_open: null pointer argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  LP_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ok();
+}
+
+int lp_ipc_close(void* dptr) {
+  if (!dptr) return fail(LP_EINVAL, "lp_ipc_close: null pointer argument");
+  LP_CUDA(cudaIpcCloseMemHandle(dptr));
+  return ok();
+}
+
+int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, void* stream) {
+  if (P < 1 || rank < 0 || rank >= P || !peer_flag) return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
+  lp::k_ep_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(peer_flag, P, rank, target);
+  LP_CHECK_LAUNCH("k_ep_barrier");
+  return ok();
+}
+
+int lp_ep_post_counts(const int32_t* counts, int32_t* const* peer_inbox, int P, int El, int rank, void* stream) {
+  if (P < 1 || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !counts || !peer_inbox)
+    return fail(LP_EINVAL, "lp_ep_post_counts: bad arguments P=%d El=%d rank=%d", P, El, rank);
+  lp::k_ep_post_counts<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(counts, peer_inbox, P, El, rank);
+  LP_CHECK_LAUNCH("k_ep_post_counts");
+  return ok();
+}
+
+int lp_ep_plan(int32_t* const* peer_inbox, int P, int El, int rank, int32_t* dest_base, int32_t* off_local,
+               void* stream) {
+  if (P < 1 || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !peer_inbox || !dest_base ||
+      !off_local)
+    return fail(LP_EINVAL, "lp_ep_plan: bad arguments P=%d El=%d rank=%d", P, El, rank);
+  const size_t sm = static_cast<size_t>(P) * P * El * sizeof(int32_t);
+  if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_plan: P*P*El too large");
+  lp::k_ep_plan<<<1, 256, sm, static_cast<cudaStream_t>(stream)>>>(peer_inbox, P, El, rank, dest_base, off_local);
+  LP_CHECK_LAUNCH("k_ep_plan");
+  return ok();
+}
+
+int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, const int32_t* offsets,
+                   const int32_t* dest_base, void* const* peer_recv, int T, int H, int topk, int El,
+                   int32_t* dest_rank, int32_t* dest_row, void* stream) {
+  if (T < 0 || H <= 0 || H % 8 || topk < 1 || El < 1) return fail(LP_EINVAL, "lp_ep_dispatch: bad shape");
+  if (T == 0) return ok();
+  if (!x || !ids || !slot_of || !offsets || !dest_base || !peer_recv || !dest_rank || !dest_row)
+    return fail(LP_EINVAL, "lp_ep_dispatch: null pointer argument");
+  const int S = T * topk;
+  lp::k_ep_dispatch<<<(S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), ids, slot_of, offsets, dest_base,
+      reinterpret_cast<__nv_bfloat16* const*>(peer_recv), S, H, topk, El, dest_rank, dest_row);
+  LP_CHECK_LAUNCH("k_ep_dispatch");
+  return ok();
+}
+
+int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* dest_row, const float* w, int T,
+                  int H, int topk, void* y, void* stream) {
+  if (T < 0 || H <= 0 || H % 8 || topk < 1 || topk > 32) return fail(LP_EINVAL, "lp_ep_combine: bad shape");
+  if (T == 0) return ok();
+  if (!peer_y || !dest_rank || !dest_row || !w || !y) return fail(LP_EINVAL, "lp_ep_combine: null pointer argument");
+  lp::k_ep_combine<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,
+      static_cast<__nv_bfloat16*>(y));
+  LP_CHECK_LAUNCH("k_ep_combine");
   return ok();
 }
 

@@ -22,6 +22,7 @@ world-size-2 gloo on CPU (tests/test_ep.py injects CPU ops there).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -182,6 +183,166 @@ class EPMoE:
             y = out
         self.last_ids, self.last_weights = ids, w
         return y, EPStats(counts, R, send_splits, recv_splits, s)
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None,
+                     x_dev: torch.Tensor | None = None):
+        """End-to-end call with host buffers: H2D copy, EP layer, D2H copy."""
+        xd = x_dev if x_dev is not None else torch.empty(x_host.shape, dtype=x_host.dtype, device=self.device)
+        xd.copy_(x_host, non_blocking=True)
+        yd, stats = self.forward(xd)
+        if y_host is None:
+            y_host = torch.empty(yd.shape, dtype=yd.dtype, pin_memory=True)
+        y_host.copy_(yd, non_blocking=True)
+        return y_host, stats
+
+
+class PeerEP:
+    """Expert-parallel MoE layer over peer memory: no collective library on the data path.
+
+    The NCCL path above moves rows with two `all_to_all_single` calls around a
+    local re-permutation. Here each rank exposes one symmetric region through
+    CUDA IPC (NVLink/NVSwitch P2P between GPUs) holding
+        [barrier counter | per-source expert counts | recv_x [cap, H] | y_out [cap, H]]
+    and every layer is (C-ABI calls, ep_p2p.cuh):
+        route + index-only permute -> post counts -> barrier -> plan (per-destination
+        row bases, own expert offsets) -> fused permute+dispatch into the owners'
+        recv_x -> barrier -> grouped experts on recv_x -> y_out -> barrier ->
+        fused receive+combine from the owners' y_out -> barrier.
+    Received rows are expert-major, source-rank-major within an expert, so the
+    owner's expert kernel runs on them directly (no re-permutation) and every
+    (token, expert) row sees exactly the math of the single-GPU layer: outputs
+    are bit-identical to GpuMoE on the same tokens (tests/test_gpu_ep_p2p.py).
+    `group` is only used once, to exchange the IPC handles (any backend).
+    """
+
+    def __init__(self, shape: MoEShape, wr: torch.Tensor, w13_local: torch.Tensor, w2_local: torch.Tensor,
+                 rank: int, world: int, max_tokens: int, group=None, share: "PeerEP | None" = None):
+        E, H, k = shape.num_experts, shape.hidden, shape.top_k
+        require(E % world == 0, f"num_experts={E} must be divisible by the EP world size {world}")
+        require(max_tokens >= 1, f"max_tokens must be >= 1, got {max_tokens}")
+        self.shape, self.rank, self.world = shape, rank, world
+        self.el = E // world
+        self.max_tokens = max_tokens
+        self.device = wr.device
+        for name, t, shp in (("wr", wr, (E, H)), ("w13_local", w13_local, (self.el, 2 * shape.ffn, H)),
+                             ("w2_local", w2_local, (self.el, H, shape.ffn))):
+            _check_tensor(name, t, shp, torch.bfloat16)
+        self.wr, self.w13, self.w2 = wr, w13_local, w2_local
+        self.lib = _native.load()
+        self.ops = GpuOps(self.device)
+        if share is not None:  # layers of one stack run in sequence: reuse the mapped region and barrier epoch
+            require(share.world == world and share.rank == rank and share.max_tokens >= max_tokens
+                    and share.shape.hidden == H and share.el == self.el, "share: incompatible PeerEP")
+            self._shared = share
+            self.cap = share.cap
+            return
+        self._shared = None
+        self.cap = max_tokens * k * world  # worst case: every rank's entries land on this rank
+        align = lambda n: (n + 255) // 256 * 256  # noqa: E731
+        self._off_flag = 0
+        self._off_inbox = 256
+        self._off_recv = align(self._off_inbox + 4 * world * self.el)
+        self._off_y = align(self._off_recv + 2 * self.cap * H)
+        total = align(self._off_y + 2 * self.cap * H)
+        self.region = torch.zeros(total, dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_size_t(0)
+        _native.check(self.lib.lp_ipc_handle(self.region.data_ptr(), handle, ctypes.byref(off)), "lp_ipc_handle")
+        mine = (bytes(handle.raw), int(off.value))
+        allh: list = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened: list[int] = []
+        bases = []
+        for q, (h, o) in enumerate(allh):
+            if q == rank:
+                bases.append(self.region.data_ptr())
+                continue
+            p = ctypes.c_void_p(0)
+            _native.check(self.lib.lp_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "lp_ipc_open")
+            self._opened.append(int(p.value))
+            bases.append(int(p.value) + o)
+        arr = lambda off: torch.tensor([b + off for b in bases], dtype=torch.int64, device=self.device)  # noqa: E731
+        self.peer_flag, self.peer_inbox = arr(self._off_flag), arr(self._off_inbox)
+        self.peer_recv, self.peer_y = arr(self._off_recv), arr(self._off_y)
+        self.recv_x = self.region[self._off_recv:self._off_recv + 2 * self.cap * H].view(torch.bfloat16).view(self.cap, H)
+        self.y_out = self.region[self._off_y:self._off_y + 2 * self.cap * H].view(torch.bfloat16).view(self.cap, H)
+        self._epoch = [0]
+        self.dest_base = torch.empty((world * self.el,), dtype=torch.int32, device=self.device)
+        self.off_local = torch.empty((self.el + 1,), dtype=torch.int32, device=self.device)
+        dist.barrier(group=group)  # every rank mapped every region before the first device barrier
+
+    def __getattr__(self, name):  # symmetric buffers of a shared region
+        shared = self.__dict__.get("_shared")
+        if shared is not None and name in ("region", "peer_flag", "peer_inbox", "peer_recv", "peer_y", "recv_x",
+                                           "y_out", "_epoch", "dest_base", "off_local", "_opened"):
+            return getattr(shared, name)
+        raise AttributeError(name)
+
+    @classmethod
+    def from_full(cls, shape: MoEShape, wr, w13, w2, rank: int, world: int, max_tokens: int, group=None,
+                  share: "PeerEP | None" = None) -> "PeerEP":
+        el = shape.num_experts // world
+        sl = slice(rank * el, (rank + 1) * el)
+        return cls(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, max_tokens, group, share)
+
+    def close(self) -> None:
+        if self._shared is not None:
+            return
+        for p in self._opened:
+            self.lib.lp_ipc_close(p)
+        self._opened = []
+
+    def _barrier(self, st) -> None:
+        self._epoch[0] += 1
+        _native.check(self.lib.lp_ep_barrier(self.peer_flag.data_ptr(), self.world, self.rank,
+                                             self.world * self._epoch[0], st), "lp_ep_barrier")
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, EPStats]:
+        s, P, el, lib = self.shape, self.world, self.el, self.lib
+        require(x.dim() == 2 and x.shape[1] == s.hidden, f"x must be [T, {s.hidden}], got {tuple(x.shape)}")
+        T, H, k = x.shape[0], s.hidden, s.top_k
+        require(T <= self.max_tokens, f"T={T} exceeds max_tokens={self.max_tokens}")
+        st = _stream_ptr(self.device)
+        ids, w = self.ops.route(x, self.wr, k, s.norm_topk_prob)
+        counts = torch.zeros((s.num_experts,), dtype=torch.int32, device=self.device)
+        offsets = torch.zeros((s.num_experts + 1,), dtype=torch.int32, device=self.device)
+        S = T * k
+        slot_of = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
+        tok_of = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
+        if T:  # index-only permutation: slots within each (global) expert, no x_perm
+            ws = self.ops._workspace(T, H, 128, s.num_experts, k)
+            _native.check(lib.lp_moe_permute(ids.data_ptr(), x.data_ptr(), T, H, s.num_experts, k, counts.data_ptr(),
+                                             offsets.data_ptr(), slot_of.data_ptr(), tok_of.data_ptr(), None,
+                                             ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
+        _native.check(lib.lp_ep_post_counts(counts.data_ptr(), self.peer_inbox.data_ptr(), P, el, self.rank, st),
+                      "lp_ep_post_counts")
+        self._barrier(st)
+        _native.check(lib.lp_ep_plan(self.peer_inbox.data_ptr(), P, el, self.rank, self.dest_base.data_ptr(),
+                                     self.off_local.data_ptr(), st), "lp_ep_plan")
+        dest_rank = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
+        dest_row = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
+        _native.check(lib.lp_ep_dispatch(x.data_ptr(), ids.data_ptr(), slot_of.data_ptr(), offsets.data_ptr(),
+                                         self.dest_base.data_ptr(), self.peer_recv.data_ptr(), T, H, k, el,
+                                         dest_rank.data_ptr(), dest_row.data_ptr(), st), "lp_ep_dispatch")
+        R = int(self.off_local[el].item())  # rows this rank's experts receive (one host sync per layer)
+        self._barrier(st)
+        if R:
+            act = torch.empty((R, s.ffn), dtype=torch.bfloat16, device=self.device)
+            ws = self.ops._workspace(R, H, s.ffn, el, 1)
+            _native.check(lib.lp_moe_experts(self.recv_x.data_ptr(), self.off_local.data_ptr(), R, self.w13.data_ptr(),
+                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), self.y_out.data_ptr(),
+                                             ws.data_ptr(), ws.numel(), st), "lp_moe_experts")
+        self._barrier(st)
+        y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
+        _native.check(lib.lp_ep_combine(self.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
+                                        w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
+        self._barrier(st)
+        self.last_ids, self.last_weights = ids, w
+        sc = counts.view(P, el).sum(1).tolist()
+        return y, EPStats(counts, R, sc, [], s)
 
     __call__ = forward
 
