@@ -113,6 +113,13 @@ int router_tile_tokens(int T, int E, int topk) {
 
 // CTAs per router token tile: split H across a cluster while the grid is small.
 int router_cluster(int ntiles, int H, int TN, int E) {
+  static const int forced = env_int("LPMOE_ROUTER_CS", 0);  // tuning knob: 1, 2 or 4
+  if (forced == 1 || forced == 2 || forced == 4) {
+    const int e_pad = (E + 31) / 32 * 32;
+    int cs = forced < (TN == lp::kRouterTileLarge ? 2 : 4) ? forced : (TN == lp::kRouterTileLarge ? 2 : 4);
+    while (cs > 1 && ((H / 64) % cs != 0 || (4 / cs) * TN * e_pad > lp::router_part_floats() || TN / cs < 4)) cs >>= 1;
+    return cs;
+  }
   int cs = 1;
   const int cs_max = TN == lp::kRouterTileLarge ? 2 : 4;
   while (cs < cs_max && ntiles * cs * 2 <= kTargetCtas && (H / 64) % (cs * 2) == 0) {
@@ -442,11 +449,12 @@ int launch_experts_pair(const void* src, int src_rows, int S, const void* act, c
 }
 
 // k-blocks of the first item's W13 warmed in L2 before pdl_wait (2 x 16 KiB each);
-// tuning knob LPMOE_PREFETCH_KB (default 16 -> 0.5 MiB per CTA).
+// tuning knob LPMOE_PREFETCH_KB (default 32 = the whole first UP item, 1 MiB per CTA;
+// B200, T=576: 210.4-211.5 vs 211.8-212.2 us at 16, e2e 208 vs 210.5).
 int prefetch_kblocks() {
   static const int v = [] {
     const char* s = getenv("LPMOE_PREFETCH_KB");
-    return s ? atoi(s) : 16;
+    return s ? atoi(s) : 32;
   }();
   return v;
 }
