@@ -127,6 +127,10 @@ int lp_profile_events(void* const* events, int n);
  * offset in it; lp_ipc_open maps a handle from ANOTHER process (peer access
  * enabled lazily) and returns the allocation base. */
 int lp_ipc_handle(const void* dptr, void* handle64, size_t* offset);
+/* Zero-filled cudaMalloc region for a rank's symmetric EP buffers (setup time,
+ * not on the layer path; IPC cannot export caching-allocator VMM segments). */
+int lp_ipc_alloc(size_t bytes, void** dptr);
+int lp_ipc_free(void* dptr);
 int lp_ipc_open(const void* handle64, void** dptr);
 int lp_ipc_close(void* dptr);
 

@@ -42,6 +42,8 @@ SIGNATURES = {
     "lp_profile_events": (_i, [_p, _i]),
     "lp_ipc_handle": (_i, [_p, _p, _p]),
     "lp_ipc_open": (_i, [_p, _p]),
+    "lp_ipc_alloc": (_i, [_sz, _p]),
+    "lp_ipc_free": (_i, [_p]),
     "lp_ipc_close": (_i, [_p]),
     "lp_ep_barrier": (_i, [_p, _i, _i, ctypes.c_uint32, _p]),
     "lp_ep_post_counts": (_i, [_p, _p, _i, _i, _i, _p]),

@@ -800,6 +800,20 @@ int lp_ipc_handle(const void* dptr, void* handle64, size_t* offset) {
   return ok();
 }
 
+int lp_ipc_alloc(size_t bytes, void** dptr) {
+  if (!dptr || bytes == 0) return fail(LP_EINVAL, "lp_ipc_alloc: bad arguments");
+  // plain cudaMalloc: IPC handles cannot name VMM (expandable-segment) allocations
+  LP_CUDA(cudaMalloc(dptr, bytes));
+  LP_CUDA(cudaMemset(*dptr, 0, bytes));
+  return ok();
+}
+
+int lp_ipc_free(void* dptr) {
+  if (!dptr) return fail(LP_EINVAL, "lp_ipc_free: null pointer argument");
+  LP_CUDA(cudaFree(dptr));
+  return ok();
+}
+
 int lp_ipc_open(const void* handle64, void** dptr) {
   if (!handle64 || !dptr) return fail(LP_EINVAL, "lp_ipc_open: null pointer argument");
   cudaIpcMemHandle_t h;

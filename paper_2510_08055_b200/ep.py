@@ -246,11 +246,12 @@ class PeerEP:
         self._off_recv = align(self._off_inbox + 4 * world * self.el)
         self._off_y = align(self._off_recv + 2 * self.cap * H)
         total = align(self._off_y + 2 * self.cap * H)
-        self.region = torch.zeros(total, dtype=torch.uint8, device=self.device)
-        torch.cuda.synchronize(self.device)
+        base = ctypes.c_void_p(0)
+        _native.check(self.lib.lp_ipc_alloc(total, ctypes.byref(base)), "lp_ipc_alloc")
+        self._region_ptr = int(base.value)
         handle = ctypes.create_string_buffer(64)
         off = ctypes.c_size_t(0)
-        _native.check(self.lib.lp_ipc_handle(self.region.data_ptr(), handle, ctypes.byref(off)), "lp_ipc_handle")
+        _native.check(self.lib.lp_ipc_handle(self._region_ptr, handle, ctypes.byref(off)), "lp_ipc_handle")
         mine = (bytes(handle.raw), int(off.value))
         allh: list = [None] * world
         dist.all_gather_object(allh, mine, group=group)
@@ -258,7 +259,7 @@ class PeerEP:
         bases = []
         for q, (h, o) in enumerate(allh):
             if q == rank:
-                bases.append(self.region.data_ptr())
+                bases.append(self._region_ptr)
                 continue
             p = ctypes.c_void_p(0)
             _native.check(self.lib.lp_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "lp_ipc_open")
@@ -267,8 +268,8 @@ class PeerEP:
         arr = lambda off: torch.tensor([b + off for b in bases], dtype=torch.int64, device=self.device)  # noqa: E731
         self.peer_flag, self.peer_inbox = arr(self._off_flag), arr(self._off_inbox)
         self.peer_recv, self.peer_y = arr(self._off_recv), arr(self._off_y)
-        self.recv_x = self.region[self._off_recv:self._off_recv + 2 * self.cap * H].view(torch.bfloat16).view(self.cap, H)
-        self.y_out = self.region[self._off_y:self._off_y + 2 * self.cap * H].view(torch.bfloat16).view(self.cap, H)
+        self.recv_x_ptr = self._region_ptr + self._off_recv  # [cap, H] bf16
+        self.y_out_ptr = self._region_ptr + self._off_y      # [cap, H] bf16
         self._epoch = [0]
         self.dest_base = torch.empty((world * self.el,), dtype=torch.int32, device=self.device)
         self.off_local = torch.empty((self.el + 1,), dtype=torch.int32, device=self.device)
@@ -276,8 +277,8 @@ class PeerEP:
 
     def __getattr__(self, name):  # symmetric buffers of a shared region
         shared = self.__dict__.get("_shared")
-        if shared is not None and name in ("region", "peer_flag", "peer_inbox", "peer_recv", "peer_y", "recv_x",
-                                           "y_out", "_epoch", "dest_base", "off_local", "_opened"):
+        if shared is not None and name in ("_region_ptr", "peer_flag", "peer_inbox", "peer_recv", "peer_y",
+                                           "recv_x_ptr", "y_out_ptr", "_epoch", "dest_base", "off_local", "_opened"):
             return getattr(shared, name)
         raise AttributeError(name)
 
@@ -294,6 +295,10 @@ class PeerEP:
         for p in self._opened:
             self.lib.lp_ipc_close(p)
         self._opened = []
+        if self._region_ptr:
+            torch.cuda.synchronize(self.device)
+            self.lib.lp_ipc_free(self._region_ptr)
+            self._region_ptr = 0
 
     def _barrier(self, st) -> None:
         self._epoch[0] += 1
@@ -332,8 +337,8 @@ class PeerEP:
         if R:
             act = torch.empty((R, s.ffn), dtype=torch.bfloat16, device=self.device)
             ws = self.ops._workspace(R, H, s.ffn, el, 1)
-            _native.check(lib.lp_moe_experts(self.recv_x.data_ptr(), self.off_local.data_ptr(), R, self.w13.data_ptr(),
-                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), self.y_out.data_ptr(),
+            _native.check(lib.lp_moe_experts(self.recv_x_ptr, self.off_local.data_ptr(), R, self.w13.data_ptr(),
+                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), self.y_out_ptr,
                                              ws.data_ptr(), ws.numel(), st), "lp_moe_experts")
         self._barrier(st)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
