@@ -449,6 +449,39 @@ def _step(st: ServingState, planner: Planner, plan: BatchPlan, cost, index: int)
                            len(plan.decode_ids), plan.prefill_tokens, plan.designated_group)
 
 
+# ---------------------------------------------------------------------------- trace I/O (workload.py:14, :145-178)
+TRACE_HEADER = "id,arrival_s,input_len,output_len"
+
+
+def export_trace(requests: list[Request], path) -> None:
+    """Write requests as the reference's trace CSV (header + one `id,arrival_s,input_len,output_len` line
+    per request, arrival written with repr so it round-trips exactly; workload.py:145-150)."""
+    with open(path, "w", encoding="utf-8") as f:
+        f.write(TRACE_HEADER + "\n")
+        for r in requests:
+            f.write(f"{r.id},{r.arrival_s!r},{r.input_len},{r.output_len}\n")
+
+
+def load_trace(path) -> list[Request]:
+    """Read a trace CSV (reference format); errors name the offending line (workload.py:153-178)."""
+    out: list[Request] = []
+    with open(path, "r", encoding="utf-8") as f:
+        for lineno, line in enumerate(f, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            if lineno == 1 and line == TRACE_HEADER:
+                continue
+            parts = line.split(",")
+            if len(parts) != 4:
+                raise ValidationError(f"{path}: line {lineno}: expected 4 comma-separated fields, got {len(parts)}")
+            try:
+                out.append(Request(int(parts[0]), float(parts[1]), int(parts[2]), int(parts[3])))
+            except ValueError as exc:  # ValidationError is a ValueError: field checks report the line too
+                raise ValidationError(f"{path}: line {lineno}: {exc}") from exc
+    return out
+
+
 # ---------------------------------------------------------------------------- summary (metrics.py)
 def percentile(samples: list[float], p: float) -> float:
     """Nearest rank: sorted[ceil(p/100 * n) - 1]."""

@@ -104,3 +104,37 @@ def test_validation_errors():
         sv.Planner("bogus")
     with pytest.raises(ValidationError):
         sv.Request(0, 0.0, 0, 1)
+
+
+# ---------------------------------------------------------------- trace CSV (workload.py:14, :145-178)
+def test_trace_roundtrip_matches_reference_bytes(tmp_path):
+    """load_trace reads the reference's export byte for byte; export_trace writes the same bytes."""
+    import os
+
+    from paper_2510_08055_b200 import serving as sv
+
+    gold = os.path.join(os.path.dirname(__file__), "golden", "trace_arxiv10.csv")
+    reqs = sv.load_trace(gold)
+    assert [r.id for r in reqs] == list(range(10))
+    assert reqs[0].input_len == 11567 and reqs[0].output_len == 385
+    out = tmp_path / "t.csv"
+    sv.export_trace(reqs, out)
+    assert out.read_bytes() == open(gold, "rb").read()
+
+
+def test_trace_errors_match_reference(tmp_path):
+    import json
+    import os
+
+    import pytest
+
+    from paper_2510_08055_b200 import serving as sv
+    from paper_2510_08055_b200.types import ValidationError
+
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "trace_errors.json")))
+    for name, case in cases.items():
+        p = tmp_path / f"{name}.csv"
+        p.write_text(case["text"])
+        with pytest.raises(ValidationError) as ei:
+            sv.load_trace(str(p))
+        assert str(ei.value).replace(str(p), "<path>") == case["message"]

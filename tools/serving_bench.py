@@ -63,6 +63,8 @@ def main():
     ap.add_argument("--config", choices=["c3", "c4", "c5"], default="c3")
     ap.add_argument("--requests", type=int, default=100)
     ap.add_argument("--prompt", type=int, default=8192)
+    ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (workload.export_trace) instead of "
+                                                 "the committed arXiv request fixture")
     a = ap.parse_args()
 
     from paper_2510_08055_b200.executor import MoEModel
@@ -84,8 +86,11 @@ def main():
             target = math.ceil(L / groups)
             run_one(stack, f"c4_layered_G{groups}", "layered", 512, target, reqs, focus=0)
     else:
-        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "plans.json")))
-        reqs = [sv.Request(i, t, li, lo) for i, t, li, lo in gold["arxiv"]["requests"][: a.requests]]
+        if a.trace:
+            reqs = sv.load_trace(a.trace)[: a.requests]
+        else:
+            gold = json.load(open(os.path.join(ROOT, "tests", "golden", "plans.json")))
+            reqs = [sv.Request(i, t, li, lo) for i, t, li, lo in gold["arxiv"]["requests"][: a.requests]]
         for policy in ("layered", "chunked"):
             run_one(stack, f"c5_{policy}", policy, 512, 512, reqs)
 
