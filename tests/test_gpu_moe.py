@@ -276,3 +276,30 @@ def test_back_to_back_layers_large_T(cuda):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("T", [576, 4100])
+def test_cuda_graph_capture_replays_layer(cuda, T):
+    """lpmoe.h promises a graph-capturable layer (no host sync, no allocation, PDL and cluster
+    launches inside): capture once, replay on new inputs, compare with eager calls bit for bit."""
+    s = QWEN3_30B_A3B
+    layer = make(s, 61, cuda)[3]
+    x_static = router_tokens(T, s.hidden, 62).to(cuda)
+    y_static = torch.empty_like(x_static)
+    side = torch.cuda.Stream(cuda)
+    side.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(side):  # warm-up off the capture: workspace, kernel attributes
+        layer(x_static, out=y_static)
+    torch.cuda.current_stream(cuda).wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer(x_static, out=y_static)
+    for seed in (63, 64):
+        x = router_tokens(T, s.hidden, seed).to(cuda)
+        x_static.copy_(x)
+        g.replay()
+        torch.cuda.synchronize()
+        ref, _ = layer(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y_static, ref)
