@@ -245,7 +245,7 @@ def run_ours(args, rank: int, world: int):
         if world > 1:
             if args.ep == "p2p":  # one symmetric IPC region shared by the layer sets (layers run in sequence)
                 layers.append(PeerEP.from_full(s, wr, w13, w2, rank, world, max_tokens=T,
-                                               share=layers[0] if layers else None))
+                                               region=layers[0].region if layers else None))
             else:
                 layers.append(EPMoE.from_full(s, wr, w13, w2, rank, world))
         else:

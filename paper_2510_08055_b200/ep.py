@@ -198,14 +198,75 @@ class EPMoE:
         return y_host, stats
 
 
+class PeerRegion:
+    """One rank's symmetric EP buffers, exported over CUDA IPC and mapped by every rank.
+
+    Layout (256-byte aligned): [barrier counter | per-source expert counts
+    (P x El int32) | recv_x [cap, H] bf16 | y_out [cap, H] bf16], allocated with
+    plain cudaMalloc (lp_ipc_alloc). `peer_*` are device arrays of the P ranks'
+    addresses of each part. The layers of one stack run in sequence and share
+    one region (and its barrier epoch). `group` is used once, to swap handles.
+    """
+
+    def __init__(self, device: torch.device, rank: int, world: int, cap: int, hidden: int, el: int, group=None):
+        self.device, self.rank, self.world, self.cap, self.hidden, self.el = device, rank, world, cap, hidden, el
+        self.lib = _native.load()
+        align = lambda n: (n + 255) // 256 * 256  # noqa: E731
+        off_flag, off_inbox = 0, 256
+        off_recv = align(off_inbox + 4 * world * el)
+        off_y = align(off_recv + 2 * cap * hidden)
+        total = align(off_y + 2 * cap * hidden)
+        base = ctypes.c_void_p(0)
+        _native.check(self.lib.lp_ipc_alloc(total, ctypes.byref(base)), "lp_ipc_alloc")
+        self.base = int(base.value)
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_size_t(0)
+        _native.check(self.lib.lp_ipc_handle(self.base, handle, ctypes.byref(off)), "lp_ipc_handle")
+        allh: list = [None] * world
+        dist.all_gather_object(allh, (bytes(handle.raw), int(off.value)), group=group)
+        self._opened: list[int] = []
+        bases = []
+        for q, (h, o) in enumerate(allh):
+            if q == rank:
+                bases.append(self.base)
+                continue
+            p = ctypes.c_void_p(0)
+            _native.check(self.lib.lp_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "lp_ipc_open")
+            self._opened.append(int(p.value))
+            bases.append(int(p.value) + o)
+        arr = lambda o: torch.tensor([b + o for b in bases], dtype=torch.int64, device=device)  # noqa: E731
+        self.peer_flag, self.peer_inbox = arr(off_flag), arr(off_inbox)
+        self.peer_recv, self.peer_y = arr(off_recv), arr(off_y)
+        self.recv_x_ptr = self.base + off_recv  # [cap, H] bf16
+        self.y_out_ptr = self.base + off_y      # [cap, H] bf16
+        self.epoch = 0
+        self.dest_base = torch.empty((world * el,), dtype=torch.int32, device=device)
+        self.off_local = torch.empty((el + 1,), dtype=torch.int32, device=device)
+        dist.barrier(group=group)  # every rank mapped every region before the first device barrier
+
+    def barrier(self, stream) -> None:
+        """Device-side barrier over the P ranks, ordered on `stream`."""
+        self.epoch += 1
+        _native.check(self.lib.lp_ep_barrier(self.peer_flag.data_ptr(), self.world, self.rank,
+                                             self.world * self.epoch, stream), "lp_ep_barrier")
+
+    def close(self) -> None:
+        for p in self._opened:
+            self.lib.lp_ipc_close(p)
+        self._opened = []
+        if self.base:
+            torch.cuda.synchronize(self.device)
+            self.lib.lp_ipc_free(self.base)
+            self.base = 0
+
+
 class PeerEP:
     """Expert-parallel MoE layer over peer memory: no collective library on the data path.
 
     The NCCL path above moves rows with two `all_to_all_single` calls around a
-    local re-permutation. Here each rank exposes one symmetric region through
-    CUDA IPC (NVLink/NVSwitch P2P between GPUs) holding
-        [barrier counter | per-source expert counts | recv_x [cap, H] | y_out [cap, H]]
-    and every layer is (C-ABI calls, ep_p2p.cuh):
+    local re-permutation. Here every rank's `PeerRegion` is mapped by every rank
+    (CUDA IPC: NVLink/NVSwitch P2P between GPUs) and each layer is (C-ABI calls,
+    ep_p2p.cuh):
         route + index-only permute -> post counts -> barrier -> plan (per-destination
         row bases, own expert offsets) -> fused permute+dispatch into the owners'
         recv_x -> barrier -> grouped experts on recv_x -> y_out -> barrier ->
@@ -214,11 +275,11 @@ class PeerEP:
     owner's expert kernel runs on them directly (no re-permutation) and every
     (token, expert) row sees exactly the math of the single-GPU layer: outputs
     are bit-identical to GpuMoE on the same tokens (tests/test_gpu_ep_p2p.py).
-    `group` is only used once, to exchange the IPC handles (any backend).
+    Pass the first layer's `.region` to the others of a stack (`region=`).
     """
 
     def __init__(self, shape: MoEShape, wr: torch.Tensor, w13_local: torch.Tensor, w2_local: torch.Tensor,
-                 rank: int, world: int, max_tokens: int, group=None, share: "PeerEP | None" = None):
+                 rank: int, world: int, max_tokens: int, group=None, region: PeerRegion | None = None):
         E, H, k = shape.num_experts, shape.hidden, shape.top_k
         require(E % world == 0, f"num_experts={E} must be divisible by the EP world size {world}")
         require(max_tokens >= 1, f"max_tokens must be >= 1, got {max_tokens}")
@@ -232,81 +293,22 @@ class PeerEP:
         self.wr, self.w13, self.w2 = wr, w13_local, w2_local
         self.lib = _native.load()
         self.ops = GpuOps(self.device)
-        if share is not None:  # layers of one stack run in sequence: reuse the mapped region and barrier epoch
-            require(share.world == world and share.rank == rank and share.max_tokens >= max_tokens
-                    and share.shape.hidden == H and share.el == self.el, "share: incompatible PeerEP")
-            self._shared = share
-            self.cap = share.cap
-            return
-        self._shared = None
-        self.cap = max_tokens * k * world  # worst case: every rank's entries land on this rank
-        align = lambda n: (n + 255) // 256 * 256  # noqa: E731
-        self._off_flag = 0
-        self._off_inbox = 256
-        self._off_recv = align(self._off_inbox + 4 * world * self.el)
-        self._off_y = align(self._off_recv + 2 * self.cap * H)
-        total = align(self._off_y + 2 * self.cap * H)
-        base = ctypes.c_void_p(0)
-        _native.check(self.lib.lp_ipc_alloc(total, ctypes.byref(base)), "lp_ipc_alloc")
-        self._region_ptr = int(base.value)
-        handle = ctypes.create_string_buffer(64)
-        off = ctypes.c_size_t(0)
-        _native.check(self.lib.lp_ipc_handle(self._region_ptr, handle, ctypes.byref(off)), "lp_ipc_handle")
-        mine = (bytes(handle.raw), int(off.value))
-        allh: list = [None] * world
-        dist.all_gather_object(allh, mine, group=group)
-        self._opened: list[int] = []
-        bases = []
-        for q, (h, o) in enumerate(allh):
-            if q == rank:
-                bases.append(self._region_ptr)
-                continue
-            p = ctypes.c_void_p(0)
-            _native.check(self.lib.lp_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "lp_ipc_open")
-            self._opened.append(int(p.value))
-            bases.append(int(p.value) + o)
-        arr = lambda off: torch.tensor([b + off for b in bases], dtype=torch.int64, device=self.device)  # noqa: E731
-        self.peer_flag, self.peer_inbox = arr(self._off_flag), arr(self._off_inbox)
-        self.peer_recv, self.peer_y = arr(self._off_recv), arr(self._off_y)
-        self.recv_x_ptr = self._region_ptr + self._off_recv  # [cap, H] bf16
-        self.y_out_ptr = self._region_ptr + self._off_y      # [cap, H] bf16
-        self._epoch = [0]
-        self.dest_base = torch.empty((world * self.el,), dtype=torch.int32, device=self.device)
-        self.off_local = torch.empty((self.el + 1,), dtype=torch.int32, device=self.device)
-        dist.barrier(group=group)  # every rank mapped every region before the first device barrier
-
-    def __getattr__(self, name):  # symmetric buffers of a shared region
-        shared = self.__dict__.get("_shared")
-        if shared is not None and name in ("_region_ptr", "peer_flag", "peer_inbox", "peer_recv", "peer_y",
-                                           "recv_x_ptr", "y_out_ptr", "_epoch", "dest_base", "off_local", "_opened"):
-            return getattr(shared, name)
-        raise AttributeError(name)
+        cap = max_tokens * k * world  # worst case: every rank's entries land on this rank
+        if region is None:
+            region = PeerRegion(self.device, rank, world, cap, H, self.el, group)
+        require(region.world == world and region.rank == rank and region.cap >= cap and region.hidden == H
+                and region.el == self.el, "region: incompatible PeerRegion for this layer")
+        self.region = region
 
     @classmethod
     def from_full(cls, shape: MoEShape, wr, w13, w2, rank: int, world: int, max_tokens: int, group=None,
-                  share: "PeerEP | None" = None) -> "PeerEP":
+                  region: PeerRegion | None = None) -> "PeerEP":
         el = shape.num_experts // world
         sl = slice(rank * el, (rank + 1) * el)
-        return cls(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, max_tokens, group, share)
-
-    def close(self) -> None:
-        if self._shared is not None:
-            return
-        for p in self._opened:
-            self.lib.lp_ipc_close(p)
-        self._opened = []
-        if self._region_ptr:
-            torch.cuda.synchronize(self.device)
-            self.lib.lp_ipc_free(self._region_ptr)
-            self._region_ptr = 0
-
-    def _barrier(self, st) -> None:
-        self._epoch[0] += 1
-        _native.check(self.lib.lp_ep_barrier(self.peer_flag.data_ptr(), self.world, self.rank,
-                                             self.world * self._epoch[0], st), "lp_ep_barrier")
+        return cls(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, max_tokens, group, region)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, EPStats]:
-        s, P, el, lib = self.shape, self.world, self.el, self.lib
+        s, P, el, lib, rg = self.shape, self.world, self.el, self.lib, self.region
         require(x.dim() == 2 and x.shape[1] == s.hidden, f"x must be [T, {s.hidden}], got {tuple(x.shape)}")
         T, H, k = x.shape[0], s.hidden, s.top_k
         require(T <= self.max_tokens, f"T={T} exceeds max_tokens={self.max_tokens}")
@@ -322,29 +324,29 @@ class PeerEP:
             _native.check(lib.lp_moe_permute(ids.data_ptr(), x.data_ptr(), T, H, s.num_experts, k, counts.data_ptr(),
                                              offsets.data_ptr(), slot_of.data_ptr(), tok_of.data_ptr(), None,
                                              ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
-        _native.check(lib.lp_ep_post_counts(counts.data_ptr(), self.peer_inbox.data_ptr(), P, el, self.rank, st),
+        _native.check(lib.lp_ep_post_counts(counts.data_ptr(), rg.peer_inbox.data_ptr(), P, el, self.rank, st),
                       "lp_ep_post_counts")
-        self._barrier(st)
-        _native.check(lib.lp_ep_plan(self.peer_inbox.data_ptr(), P, el, self.rank, self.dest_base.data_ptr(),
-                                     self.off_local.data_ptr(), st), "lp_ep_plan")
+        rg.barrier(st)
+        _native.check(lib.lp_ep_plan(rg.peer_inbox.data_ptr(), P, el, self.rank, rg.dest_base.data_ptr(),
+                                     rg.off_local.data_ptr(), st), "lp_ep_plan")
         dest_rank = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
         dest_row = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
         _native.check(lib.lp_ep_dispatch(x.data_ptr(), ids.data_ptr(), slot_of.data_ptr(), offsets.data_ptr(),
-                                         self.dest_base.data_ptr(), self.peer_recv.data_ptr(), T, H, k, el,
+                                         rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(), T, H, k, el,
                                          dest_rank.data_ptr(), dest_row.data_ptr(), st), "lp_ep_dispatch")
-        R = int(self.off_local[el].item())  # rows this rank's experts receive (one host sync per layer)
-        self._barrier(st)
+        R = int(rg.off_local[el].item())  # rows this rank's experts receive (one host sync per layer)
+        rg.barrier(st)
         if R:
             act = torch.empty((R, s.ffn), dtype=torch.bfloat16, device=self.device)
             ws = self.ops._workspace(R, H, s.ffn, el, 1)
-            _native.check(lib.lp_moe_experts(self.recv_x_ptr, self.off_local.data_ptr(), R, self.w13.data_ptr(),
-                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), self.y_out_ptr,
+            _native.check(lib.lp_moe_experts(rg.recv_x_ptr, rg.off_local.data_ptr(), R, self.w13.data_ptr(),
+                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), rg.y_out_ptr,
                                              ws.data_ptr(), ws.numel(), st), "lp_moe_experts")
-        self._barrier(st)
+        rg.barrier(st)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
-        _native.check(lib.lp_ep_combine(self.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
+        _native.check(lib.lp_ep_combine(rg.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
                                         w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
-        self._barrier(st)
+        rg.barrier(st)
         self.last_ids, self.last_weights = ids, w
         sc = counts.view(P, el).sum(1).tolist()
         return y, EPStats(counts, R, sc, [], s)

@@ -51,7 +51,7 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
         w13, w2 = w13.to(dev), w2.to(dev)
         T = tokens[rank]
         ep = PeerEP.from_full(s, wr, w13, w2, rank, world, max_tokens=max(tokens))
-        ep2 = PeerEP.from_full(s, wr, w13, w2, rank, world, max_tokens=max(tokens), share=ep)  # same region
+        ep2 = PeerEP.from_full(s, wr, w13, w2, rank, world, max_tokens=max(tokens), region=ep.region)
         ref = GpuMoE(s, wr, w13, w2)
         ok = True
         for it in range(layers):
@@ -65,7 +65,7 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
         dist.all_reduce(rows)
         ok &= int(rows.item()) == sum(tokens) * s.top_k  # every routing entry landed exactly once
         dist.barrier()
-        ep.close()
+        ep.region.close()
         dist.destroy_process_group()
         q.put((rank, ok, ""))
     except Exception as e:  # report instead of hanging the parent
