@@ -321,17 +321,20 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
         for (int kb = 0; kb < p.H / kTileK; ++kb) {
           PW_LOCAL(&empty[stage], phase ^ 1, "gather:empty");
+          cp_async_wait_group<S_ - 1>();  // this slot's previous copies (S_ groups ago) landed
           const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + 2 * kATileBytes) + sw;
 #pragma unroll
           for (int i = 0; i < RPT; ++i)
             if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
           cp_async_arrive_noinc(&bfull[stage]);
+          cp_async_commit();
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
       } else {  // DN items: B comes by TMA; keep bfull's phases in step
         for (int kb = 0; kb < p.I / kTileK; ++kb) {
           PW_LOCAL(&empty[stage], phase ^ 1, "gather:empty");
           mbar_arrive(&bfull[stage]);
+          cp_async_commit();  // (empty group: one group per stage)
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
       }

@@ -86,6 +86,13 @@ __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src, u
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "l"(policy)
                : "memory");
 }
+// cp.async groups: one per ring stage; waiting until at most N groups are pending
+// orders this thread's reuse of a slot after its previous copies into it landed.
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 // Arrive on `bar` once every cp.async this thread issued so far has landed;
 // .noinc: the arrival counts toward the barrier's expected count.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
