@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=T_DECODE + T_PREFILL)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shape", choices=["qwen", "gptoss"], default="qwen",
+                    help="layer shape: Qwen3-30B-A3B (the BASELINE metric) or the reference's GPT-OSS-20B config")
     ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 exchange: fused dispatch/combine over peer memory (ep.PeerEP) or NCCL all_to_all")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -222,7 +224,7 @@ def run_ours(args, rank: int, world: int):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_08055_b200 import QWEN3_30B_A3B as s
+    from paper_2510_08055_b200 import GPT_OSS_20B, QWEN3_30B_A3B
     from paper_2510_08055_b200 import _native
     from paper_2510_08055_b200.moe import GpuMoE
     from paper_2510_08055_b200.synthetic import router_tokens, router_weight
@@ -232,6 +234,7 @@ def run_ours(args, rank: int, world: int):
     dev = torch.device("cuda", local)
     clocks = ClockSampler(local).start()
     T = args.tokens
+    s = GPT_OSS_20B if args.shape == "gptoss" else QWEN3_30B_A3B
     lib = _native.load()
 
     if world > 1:
@@ -376,10 +379,13 @@ def run_ours(args, rank: int, world: int):
         return
     peak, peak_src = measured_peaks()
     out = {
-        "metric": METRIC, "value": ms * 1e3, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "metric": METRIC if args.shape == "qwen" else METRIC.replace("Qwen3-30B-A3B", "GPT-OSS-20B shape"),
+        "value": ms * 1e3, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init Qwen3-30B-A3B-shaped weights, dyadic-grid tokens)",
-        "config": {"workload": f"qwen3-30b-a3b MoE layer, T={T} ({T_DECODE} decode + {T - T_DECODE} prefill)",
+        "data": f"synthetic (random-init {'Qwen3-30B-A3B' if args.shape == 'qwen' else 'GPT-OSS-20B'}-shaped "
+                "weights, dyadic-grid tokens)",
+        "config": {"workload": f"{'qwen3-30b-a3b' if args.shape == 'qwen' else 'gpt-oss-20b-shaped'} MoE layer, "
+                               f"T={T} ({min(T, T_DECODE)} decode + {max(T - T_DECODE, 0)} prefill)",
                    "tokens": T, "hidden": s.hidden, "ffn": s.ffn, "experts": s.num_experts, "top_k": s.top_k,
                    "parallelism": f"ep{world}" if world > 1 else "single",
                    "ep_exchange": (("peer-memory fused dispatch/combine (CUDA IPC, NVLink P2P)" if args.ep == "p2p"

@@ -21,7 +21,7 @@
  *    and its own workspace.
  *  - Layouts (HF Qwen3-MoE, transformers 5.5 modeling_qwen3_moe.py:220-224,
  *    :255): x, y [T,H]; wr [E,H]; w13 [E,2I,H] (gate rows 0..I-1, up rows
- *    I..2I-1); w2 [E,H,I]. Constraints: H%128==0, I%128==0, E<=256,
+ *    I..2I-1); w2 [E,H,I]. Constraints: H%64==0, I%64==0, E<=256,
  *    1<=topk<=min(E,32).
  */
 #ifndef LPMOE_H_

@@ -6,6 +6,6 @@ FFN and combine on sm_100a through the C ABI in include/lpmoe.h, plus the
 reference-facing adapters (coverage models, union-count sampler).
 """
 
-from .types import MoEShape, ModelSpec, QWEN3_30B_A3B, TINY, ValidationError  # noqa: F401
+from .types import GPT_OSS_20B, MoEShape, ModelSpec, QWEN3_30B_A3B, TINY, ValidationError  # noqa: F401
 
 __version__ = "0.1.0"

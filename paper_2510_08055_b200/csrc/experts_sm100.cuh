@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     // While the predecessors (router / scan / gather) finish, warm L2 with the
     // first k-blocks of this CTA's first work item (item == blockIdx.x), guessed
     // assuming one token tile per expert — exact in the memory-bound regime.
-    const int mt_up0 = p.I / kTileM;
+    const int mt_up0 = (p.I + kTileM - 1) / kTileM;
     const int e_guess = blockIdx.x / mt_up0;
     if (e_guess < E && e_guess * 2 * p.I + 2 * p.I > p.warm_rows) {
       const int row = e_guess * 2 * p.I + (blockIdx.x % mt_up0) * kTileM;
@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int mt_up = p.I / kTileM;
+  // I and H need only be multiples of 64 (one k-block): a last partial 128-row
+  // tile reads into the next rows (or TMA zero fill) and its extra features are
+  // never stored (epilogue masks feat >= I / H).
+  const int mt_up = (p.I + kTileM - 1) / kTileM;
   const int mt_dn = (p.H + 2 * kTileM - 1) / (2 * kTileM);
   const int total_tiles = s_tp[E];
   const int n_up = mt_up * total_tiles;
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       const int feat = m0 + 32 * q + lane;  // output feature owned by this thread
       const int nchunks = (nvalid + 15) / 16;
       if (kind == kItemUp) {
+        const bool fok = feat < p.I;
         __nv_bfloat16* dst = p.act + static_cast<size_t>(row0) * p.I + feat;
         for (int c = half; c < nchunks; c += 2) {
           uint32_t g[16], u[16];
@@ -470,13 +474,14 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int n = c * 16 + i;
-            if (n < nvalid)
+            if (n < nvalid && fok)
               dst[static_cast<size_t>(n) * p.I] =
                   __float2bfloat16_rn(silu_mul(__uint_as_float(g[i]), __uint_as_float(u[i])));
           }
         }
       } else {
         const bool two = m0 + kTileM < p.H;
+        const bool fok = feat < p.H, fok2 = feat + kTileM < p.H;
         __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
         for (int c = half; c < nchunks; c += 2) {
           uint32_t v[16], v2[16];
@@ -487,8 +492,8 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           for (int i = 0; i < 16; ++i) {
             const int n = c * 16 + i;
             if (n < nvalid) {
-              dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
-              if (two) dst[static_cast<size_t>(n) * p.H + kTileM] = __float2bfloat16_rn(__uint_as_float(v2[i]));
+              if (fok) dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
+              if (two && fok2) dst[static_cast<size_t>(n) * p.H + kTileM] = __float2bfloat16_rn(__uint_as_float(v2[i]));
             }
           }
         }

@@ -165,8 +165,8 @@ Layout make_layout(int T, int H, int I, int E, int topk) {
 
 int check_dims(int T, int H, int I, int E, int topk) {
   if (T < 0 || T > kMaxTokens) return fail(LP_EINVAL, "T must be in [0, %d], got %d", kMaxTokens, T);
-  if (H <= 0 || H % 128) return fail(LP_EINVAL, "H must be a positive multiple of 128, got %d", H);
-  if (I <= 0 || I % 128) return fail(LP_EINVAL, "I must be a positive multiple of 128, got %d", I);
+  if (H <= 0 || H % 64) return fail(LP_EINVAL, "H must be a positive multiple of 64, got %d", H);
+  if (I <= 0 || I % 64) return fail(LP_EINVAL, "I must be a positive multiple of 64, got %d", I);
   if (E < 1) return fail(LP_EINVAL, "E must be >= 1, got %d", E);
   if (E > lp::kMaxExperts) return fail(LP_EUNSUPPORTED, "E > %d not supported, got %d", lp::kMaxExperts, E);
   if (topk < 1 || topk > E) return fail(LP_EINVAL, "topk out of range: need 1 <= topk <= E, got %d", topk);

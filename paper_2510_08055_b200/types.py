@@ -67,8 +67,8 @@ class MoEShape:
     norm_topk_prob: bool = True
 
     def __post_init__(self):
-        require(self.hidden > 0 and self.hidden % 128 == 0, f"hidden must be a positive multiple of 128, got {self.hidden}")
-        require(self.ffn > 0 and self.ffn % 128 == 0, f"ffn must be a positive multiple of 128, got {self.ffn}")
+        require(self.hidden > 0 and self.hidden % 64 == 0, f"hidden must be a positive multiple of 64, got {self.hidden}")
+        require(self.ffn > 0 and self.ffn % 64 == 0, f"ffn must be a positive multiple of 64, got {self.ffn}")
         require(1 <= self.num_experts <= 256, f"num_experts must be in [1, 256], got {self.num_experts}")
         require(
             1 <= self.top_k <= min(self.num_experts, 32),
@@ -95,6 +95,17 @@ class MoEShape:
 # Shapes named by BASELINE.json
 QWEN3_30B_A3B = MoEShape(hidden=2048, ffn=768, num_experts=128, top_k=8, norm_topk_prob=True)
 TINY = MoEShape(hidden=256, ffn=128, num_experts=16, top_k=2, norm_topk_prob=True)
+
+# The reference's second model config (configs/gptoss20b.toml: hidden 2880, MoE
+# intermediate 2880, 32 experts top-4; bytes_per_expert 49,766,400 = 3*2880*2880*2).
+# Shape only: the layer math is the Qwen3-MoE one (router softmax/top-k, SiLU*mul).
+GPT_OSS_20B = MoEShape(hidden=2880, ffn=2880, num_experts=32, top_k=4, norm_topk_prob=True)
+
+GPT_OSS_20B_MODEL = ModelSpec(
+    name="gptoss-20b", num_layers=24, num_experts=32, top_k=4, bytes_per_expert=49766400,
+    dense_bytes_per_layer=53268480, flops_per_token_per_expert=49766400, attn_flops_per_token_per_ctx=393216,
+    kv_bytes_per_token=32768, hidden_dim=2880, dtype_bytes=2,
+)
 
 QWEN3_30B_A3B_MODEL = ModelSpec(
     name="qwen30b-a3b", num_layers=48, num_experts=128, top_k=8, bytes_per_expert=9437184,

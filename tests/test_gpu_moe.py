@@ -81,6 +81,15 @@ def test_qwen_layer(cuda, T):
         assert stats.experts_hit == 128
 
 
+@pytest.mark.parametrize("T", [1, 64, 576, 2000])
+def test_gpt_oss_shaped_layer(cuda, T):
+    """The reference's second model config (configs/gptoss20b.toml): H = I = 2880 (not multiples of
+    128: partial last weight tiles, odd k-block count), 32 experts top-4."""
+    from paper_2510_08055_b200 import GPT_OSS_20B
+
+    check_layer(GPT_OSS_20B, T, 71, cuda)
+
+
 def test_qwen_layer_compute_bound(cuda):
     # designated-group layer of config 3 at reduced size (tokens/expert > 256 -> multi tile)
     check_layer(QWEN3_30B_A3B, 4608, 31, cuda)
