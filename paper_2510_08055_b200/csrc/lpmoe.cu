@@ -107,7 +107,8 @@ constexpr int kRouterLargeTiles = 149;  // > one wave of 16-token tiles on 148 S
 int router_tile_tokens(int T, int E, int topk) {
   static const int forced = env_int("LPMOE_ROUTER_TN", 0);
   if (forced == 16 || forced == 64) return (forced == 64 && topk > 8) ? 16 : forced;
-  if (topk > 8 || E > 256) return lp::kRouterN;
+  // 64-token tiles need 6 x (16 KiB per 128 experts + 8 KiB) of ring: one m-tile (E <= 128) only
+  if (topk > 8 || E > 128) return lp::kRouterN;
   return (T + lp::kRouterN - 1) / lp::kRouterN >= kRouterLargeTiles ? lp::kRouterTileLarge : lp::kRouterN;
 }
 

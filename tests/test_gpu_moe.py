@@ -90,6 +90,12 @@ def test_gpt_oss_shaped_layer(cuda, T):
     check_layer(GPT_OSS_20B, T, 71, cuda)
 
 
+def test_max_experts_large_batch(cuda):
+    """E = 256 (two router m-tiles) at a batch large enough for 64-token router tiles: the router
+    must keep 16-token tiles there (a 64-token ring would need 247 KB of shared memory)."""
+    check_layer(MoEShape(512, 256, 256, 8, False), 3001, 91, cuda)
+
+
 def test_qwen_layer_compute_bound(cuda):
     # designated-group layer of config 3 at reduced size (tokens/expert > 256 -> multi tile)
     check_layer(QWEN3_30B_A3B, 4608, 31, cuda)
