@@ -34,7 +34,7 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
     try:
         import torch.distributed as dist
 
-        from paper_2510_08055_b200 import QWEN3_30B_A3B, TINY
+        from paper_2510_08055_b200 import QWEN3_30B_A3B, TINY, MoEShape
         from paper_2510_08055_b200.ep import PeerEP
         from paper_2510_08055_b200.moe import GpuMoE
         from paper_2510_08055_b200.synthetic import expert_weights, router_tokens, router_weight
@@ -42,7 +42,7 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
         torch.cuda.set_device(0)
         dev = torch.device("cuda", 0)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-        s = {"tiny": TINY, "qwen": QWEN3_30B_A3B}[shape_name]
+        s = {"tiny": TINY, "qwen": QWEN3_30B_A3B, "e256": MoEShape(512, 256, 256, 8, False)}[shape_name]
         wr = router_weight(s.num_experts, s.hidden, 21).float()
         if skew:  # every token of every rank prefers the experts of rank 0
             wr[: s.top_k, s.hidden - 1] = 16.0
@@ -109,3 +109,9 @@ def test_peer_ep2_qwen_matches_single_gpu(cuda):
 
 def test_peer_ep2_skewed_to_rank0_and_empty_rank(cuda):
     _run("tiny", [80, 0], skew=True)
+
+
+def test_peer_ep2_large_uneven_batches_max_experts(cuda):
+    """E = 256 (128 per rank), 3001 vs 7 tokens: the owners' expert kernels run large
+    expert-major receive buffers (CTA-pair kernel through the staged API)."""
+    _run("e256", [3001, 7], layers=1)
