@@ -86,8 +86,7 @@ int pick_max_n(int S, int E) {
 // expert kernel's scheduler words. Must be zero-filled once after allocation;
 // every kernel leaves it zeroed again.
 constexpr int kMaxTokens = 262144;
-constexpr size_t kTicketOff = 0;
-constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB of tickets
+constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB reserved (formerly router tickets)
 constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E+1 <= 257)
 constexpr size_t kGbarOff = kSchedOff + 2048;                // fused router grid barrier (2 words)
 

@@ -119,27 +119,27 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
       psum += pr;
       if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
     }
-    return;
-  }
-  for (int r = 0; r < topk; ++r) {
-    float bv = -INFINITY;
-    int bj = -1;
+  } else {
+    for (int r = 0; r < topk; ++r) {
+      float bv = -INFINITY;
+      int bj = -1;
 #pragma unroll
-    for (int j = 0; j < NV; ++j)  // ascending expert index: the first maximum wins ties
-      if (sub + LPT * j < E && !((taken >> j) & 1u) && (bj < 0 || l[j] > bv)) { bv = l[j]; bj = j; }
-    int bi = bj >= 0 ? sub + LPT * bj : 0x7fffffff;
+      for (int j = 0; j < NV; ++j)  // ascending expert index: the first maximum wins ties
+        if (sub + LPT * j < E && !((taken >> j) & 1u) && (bj < 0 || l[j] > bv)) { bv = l[j]; bj = j; }
+      int bi = bj >= 0 ? sub + LPT * bj : 0x7fffffff;
 #pragma unroll
-    for (int o = 1; o < LPT; o <<= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi) || bi == 0x7fffffff) {
-        if (oi != 0x7fffffff) { bv = ov; bi = oi; }
+      for (int o = 1; o < LPT; o <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi) || bi == 0x7fffffff) {
+          if (oi != 0x7fffffff) { bv = ov; bi = oi; }
+        }
       }
+      if (bi % LPT == sub) taken |= 1u << (bi / LPT);
+      const float pr = __expf(bv - m) * inv;
+      psum += pr;
+      if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
     }
-    if (bi % LPT == sub) taken |= 1u << (bi / LPT);
-    const float pr = __expf(bv - m) * inv;
-    psum += pr;
-    if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
   }
 }
 
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
   const int kb_part = kb_total / npart;     // k-blocks per partial sum
   const int kb_per = ppc * kb_part;
   const int kb0 = cr * kb_per;
-  const bool tr = blockIdx.x == 0;
+  [[maybe_unused]] const bool tr = blockIdx.x == 0;  // trace builds only
   if (threadIdx.x == 0) { LP_TRACE_AT(tr, 0); LP_TRACE_MIN(8); }
 
   if (threadIdx.x == 0) {
