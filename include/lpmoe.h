@@ -77,6 +77,14 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
  * tokens/expert <= the tile cap (the moe_cost byte model, costmodel.py:77). */
 int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void* w13, const void* w2, int H,
                    int I, int E, void* act, void* y_perm, void* ws, size_t ws_bytes, void* stream);
+/* As lp_moe_experts, with the row count left on the device: x_perm / act /
+ * y_perm hold S rows (capacity), offsets[E] <= S rows are valid, and S_hint
+ * (the expected routed rows, e.g. T*topk of the sender ranks) picks the token
+ * tile width. No host read of offsets: the expert-parallel layer stays
+ * stream-ordered and graph-capturable. */
+int lp_moe_experts_rows(const void* x_perm, const int32_t* offsets, int S, int S_hint, const void* w13,
+                        const void* w2, int H, int I, int E, void* act, void* y_perm, void* ws, size_t ws_bytes,
+                        void* stream);
 
 /* K4 — weighted combine y[t] = sum_j w[t,j] * y_perm[slot_of[t,j]] (bf16 out). */
 int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, int T, int H, int topk, void* y,

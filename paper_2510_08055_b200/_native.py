@@ -34,6 +34,7 @@ SIGNATURES = {
     "lp_moe_route": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _sz, _p]),
     "lp_moe_permute": (_i, [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "lp_moe_experts": (_i, [_p, _p, _i, _p, _p, _i, _i, _i, _p, _p, _p, _sz, _p]),
+    "lp_moe_experts_rows": (_i, [_p, _p, _i, _i, _p, _p, _i, _i, _i, _p, _p, _p, _sz, _p]),
     "lp_moe_combine": (_i, [_p, _p, _p, _i, _i, _i, _p, _p]),
     "lp_moe_forward": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _sz, _p]),
     "lp_union_counts_uniform": (_i, [_p, _i, _i, _i, _i, _p, _p]),

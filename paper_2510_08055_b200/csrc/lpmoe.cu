@@ -624,11 +624,12 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   return ok();
 }
 
-int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void* w13, const void* w2, int H, int I,
-                   int E, void* act, void* y_perm, void* ws, size_t ws_bytes, void* stream) {
+int lp_moe_experts_rows(const void* x_perm, const int32_t* offsets, int S, int S_hint, const void* w13,
+                        const void* w2, int H, int I, int E, void* act, void* y_perm, void* ws, size_t ws_bytes,
+                        void* stream) {
   int rc;
   if ((rc = check_dims(0, H, I, E, 1))) return rc;
-  if (S < 0) return fail(LP_EINVAL, "S must be >= 0, got %d", S);
+  if (S < 0 || S_hint < 0) return fail(LP_EINVAL, "S and S_hint must be >= 0, got %d, %d", S, S_hint);
   if (S == 0) return ok();
   if (!x_perm || !offsets || !w13 || !w2 || !act || !y_perm || !ws)
     return fail(LP_EINVAL, "lp_moe_experts: null pointer argument");
@@ -641,7 +642,7 @@ int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void
   int32_t* tile_prefix = at<int32_t>(ws, kHeaderBytes);
   int32_t* tile_rows = at<int32_t>(ws, kHeaderBytes + blk);
   uint32_t* sched = at<uint32_t>(ws, kSchedOff);
-  const int max_n = pick_max_n(S, E);
+  const int max_n = pick_max_n(S_hint > 0 ? S_hint : S, E);
   const int sb = (E + 31) / 32 * 32;
   k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
   LP_CHECK_LAUNCH("k_plan");
@@ -650,6 +651,11 @@ int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void
                            st)))
     return rc;
   return ok();
+}
+
+int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void* w13, const void* w2, int H, int I,
+                   int E, void* act, void* y_perm, void* ws, size_t ws_bytes, void* stream) {
+  return lp_moe_experts_rows(x_perm, offsets, S, S, w13, w2, H, I, E, act, y_perm, ws, ws_bytes, stream);
 }
 
 int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, int T, int H, int topk, void* y,

@@ -103,8 +103,8 @@ class GpuOps:
 @dataclass
 class EPStats:
     counts: torch.Tensor       # int32 [E] global-expert counts of this rank's tokens
-    recv_rows: int             # rows this rank's experts processed
-    send_splits: list[int]
+    recv_rows: "int | torch.Tensor"    # rows this rank's experts processed (PeerEP: a device scalar, no sync)
+    send_splits: "list[int] | torch.Tensor"
     recv_splits: list[int]
     shape: MoEShape
 
@@ -240,9 +240,16 @@ class PeerRegion:
         self.recv_x_ptr = self.base + off_recv  # [cap, H] bf16
         self.y_out_ptr = self.base + off_y      # [cap, H] bf16
         self.epoch = 0
+        self._act: torch.Tensor | None = None
         self.dest_base = torch.empty((world * el,), dtype=torch.int32, device=device)
         self.off_local = torch.empty((el + 1,), dtype=torch.int32, device=device)
         dist.barrier(group=group)  # every rank mapped every region before the first device barrier
+
+    def act(self, ffn: int) -> torch.Tensor:
+        """Local [cap, ffn] bf16 scratch for the experts' SiLU(g)*u rows (shared by the stack)."""
+        if self._act is None or self._act.shape[1] != ffn:
+            self._act = torch.empty((self.cap, ffn), dtype=torch.bfloat16, device=self.device)
+        return self._act
 
     def barrier(self, stream) -> None:
         """Device-side barrier over the P ranks, ordered on `stream`."""
@@ -334,22 +341,22 @@ class PeerEP:
         _native.check(lib.lp_ep_dispatch(x.data_ptr(), ids.data_ptr(), slot_of.data_ptr(), offsets.data_ptr(),
                                          rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(), T, H, k, el,
                                          dest_rank.data_ptr(), dest_row.data_ptr(), st), "lp_ep_dispatch")
-        R = int(rg.off_local[el].item())  # rows this rank's experts receive (one host sync per layer)
         rg.barrier(st)
-        if R:
-            act = torch.empty((R, s.ffn), dtype=torch.bfloat16, device=self.device)
-            ws = self.ops._workspace(R, H, s.ffn, el, 1)
-            _native.check(lib.lp_moe_experts(rg.recv_x_ptr, rg.off_local.data_ptr(), R, self.w13.data_ptr(),
-                                             self.w2.data_ptr(), H, s.ffn, el, act.data_ptr(), rg.y_out_ptr,
-                                             ws.data_ptr(), ws.numel(), st), "lp_moe_experts")
+        # rows received stay on the device (off_local[El]): capacity-sized launch, tile width from the
+        # expected T*k rows; no host sync, so the whole layer is stream-ordered and graph-capturable
+        act = rg.act(s.ffn)
+        ws = self.ops._workspace(1, H, s.ffn, el, 1)  # header + tile plan only (rows live in the region)
+        _native.check(lib.lp_moe_experts_rows(rg.recv_x_ptr, rg.off_local.data_ptr(), rg.cap, max(T, 1) * k,
+                                              self.w13.data_ptr(), self.w2.data_ptr(), H, s.ffn, el,
+                                              act.data_ptr(), rg.y_out_ptr, ws.data_ptr(), ws.numel(), st),
+                      "lp_moe_experts_rows")
         rg.barrier(st)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
         _native.check(lib.lp_ep_combine(rg.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
                                         w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
         rg.barrier(st)
         self.last_ids, self.last_weights = ids, w
-        sc = counts.view(P, el).sum(1).tolist()
-        return y, EPStats(counts, R, sc, [], s)
+        return y, EPStats(counts, rg.off_local[el], counts.view(P, el).sum(1), [], s)
 
     __call__ = forward
 

@@ -61,7 +61,7 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
             torch.cuda.synchronize()
             ok &= bool(torch.equal(y, y_ref))
             ok &= bool(torch.equal(st.counts, st_ref.counts))
-        rows = torch.tensor([st.recv_rows], dtype=torch.int64)
+        rows = torch.tensor([int(st.recv_rows)], dtype=torch.int64)
         dist.all_reduce(rows)
         ok &= int(rows.item()) == sum(tokens) * s.top_k  # every routing entry landed exactly once
         dist.barrier()
