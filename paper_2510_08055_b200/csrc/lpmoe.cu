@@ -16,6 +16,7 @@
 #include "../../include/lpmoe.h"
 #include "experts_sm100.cuh"
 #include "experts_pair_sm100.cuh"
+#include "experts_tiny_sm100.cuh"
 #include "ep_p2p.cuh"
 #include "norm.cuh"
 #include "permute.cuh"
@@ -448,6 +449,29 @@ int launch_experts_pair(const void* src, int src_rows, int S, const void* act, c
   return LP_OK;
 }
 
+// Decode-size batches (<= 1 routed token per expert on average): half-size
+// items on more SMs (experts_tiny_sm100.cuh). LPMOE_TINY=0 disables.
+bool use_tiny(int S, int E, int H, int I) {
+  static const int v = env_int("LPMOE_TINY", 1);
+  return v != 0 && S <= E && H % 64 == 0 && I % 64 == 0;
+}
+
+int launch_experts_tiny(const void* x, const int32_t* tok_of, int S, const void* act, const void* w13, const void* w2,
+                        int H, int I, int E, lp::ExpertsParams p, cudaStream_t st) {
+  int rc;
+  if ((rc = get_encode())) return rc;
+  CUtensorMap tm_w13h, tm_w2, tm_act;
+  if ((rc = make_tmap(&tm_w13h, w13, static_cast<uint64_t>(E) * 2 * I, H, 64))) return rc;
+  if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_act, act, S, I, lp::TinyCfg::kN))) return rc;
+  constexpr int smem = lp::TinyCfg::kSmemBytes;
+  if ((rc = set_smem(lp::k_experts_tiny, smem))) return rc;
+  p.xsrc = static_cast<const __nv_bfloat16*>(x);
+  p.tok_of = tok_of;
+  LP_CUDA(launch_pdl(lp::k_experts_tiny, sm_count(), lp::TinyCfg::kThreads, smem, st, tm_w13h, tm_w2, tm_act, p));
+  return LP_OK;
+}
+
 // k-blocks of the first item's W13 warmed in L2 before pdl_wait (2 x 16 KiB each);
 // tuning knob LPMOE_PREFETCH_KB (default 32 = the whole first UP item, 1 MiB per CTA;
 // B200, T=576: 210.4-211.5 vs 211.8-212.2 us at 16, e2e 208 vs 210.5).
@@ -688,13 +712,14 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   if (!w) w = at<float>(ws, L.w);
   if (!counts) counts = at<int32_t>(ws, L.counts);
   const int S = T * topk;
-  const int max_n = pick_max_n(S, E);
+  const bool tiny = !use_fused_combine() && use_gather(pick_max_n(S, E)) && use_tiny(S, E, H, I);
+  const int max_n = tiny ? lp::TinyCfg::kN : pick_max_n(S, E);
   int32_t* offsets = at<int32_t>(ws, L.offsets);
   int32_t* slot_of = at<int32_t>(ws, L.slot_of);
   int32_t* tok_of = at<int32_t>(ws, L.tok_of);
   // Token rows reach the expert kernel either materialised in slot order
   // (x_perm, one scatter pass) or gathered straight from x by TMA (tok_of).
-  const bool gather = use_gather(max_n);
+  const bool gather = tiny || use_gather(max_n);
   const bool fused = use_fused_combine();
   const bool fused_route = !fused && fused_route_ok(L, T, E);
   const size_t warm = l2_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);
@@ -719,7 +744,12 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   FusedCombine fc;
   if (fused) fc = FusedCombine{y, tok_of, slot_of, w, at<uint32_t>(ws, L.blk_cnt), topk};
   prof_mark(2, st);
-  if ((rc = launch_experts(gather ? x : at<void>(ws, L.x_perm), gather ? T : S, gather ? tok_of : nullptr, S, w13,
+  if (tiny) {
+    const lp::ExpertsParams p{H, I, E, tok_of, offsets, at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                              at<__nv_bfloat16>(ws, L.act), at<__nv_bfloat16>(ws, L.y_perm), at<uint32_t>(ws, L.sched),
+                              0, 0, 0, env_wpol(), nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+    if ((rc = launch_experts_tiny(x, tok_of, S, at<void>(ws, L.act), w13, w2, H, I, E, p, st))) return rc;
+  } else if ((rc = launch_experts(gather ? x : at<void>(ws, L.x_perm), gather ? T : S, gather ? tok_of : nullptr, S, w13,
                            w2, H, I, E, max_n, offsets,
                            at<int32_t>(ws, L.tile_prefix),
                            at<int32_t>(ws, L.tile_rows), at<uint32_t>(ws, L.sched), at<void>(ws, L.act),

@@ -77,10 +77,14 @@ __device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t nblocks) {
 }
 
 // Softmax + top-k of one token held by LPT consecutive lanes (lane `sub` owns
-// experts sub, sub+LPT, ...). Writes the k ids / probabilities to smem.
+// experts sub, sub+LPT, ...). Writes the k ids and their unnormalised
+// exp(logit - max) to smem; psum = their sum in selection order, inv = 1 / the
+// full softmax denominator. With renormalisation the weights are
+// exp_r / psum: independent of LPT (the lane split changes with the router's
+// tile shape), so a token's weights are bit-identical for every batch size.
 template <int LPT, int NV>
 __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, int sub, int32_t* out_ids, float* out_p,
-                                           float& psum) {
+                                           float& psum, float& inv_out) {
   float l[NV];
   float m = -INFINITY;
 #pragma unroll
@@ -98,6 +102,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
 #pragma unroll
   for (int o = 1; o < LPT; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
   const float inv = 1.0f / ssum;
+  inv_out = inv;
   uint32_t taken = 0;
   psum = 0.f;
   if constexpr (LPT == 32) {
@@ -115,7 +120,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
       const int bi = static_cast<int>(__reduce_min_sync(0xffffffffu, cand));
       if ((bi & 31) == sub) taken |= 1u << (bi >> 5);
       const uint32_t vb = (kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax;
-      const float pr = __expf(__uint_as_float(vb) - m) * inv;
+      const float pr = __expf(__uint_as_float(vb) - m);
       psum += pr;
       if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
     }
@@ -136,7 +141,7 @@ __device__ __forceinline__ void topk_lanes(const float* row, int E, int topk, in
         }
       }
       if (bi % LPT == sub) taken |= 1u << (bi / LPT);
-      const float pr = __expf(bv - m) * inv;
+      const float pr = __expf(bv - m);
       psum += pr;
       if (sub == 0) { out_ids[r] = bi; out_p[r] = pr; }
     }
@@ -344,13 +349,13 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
       if (g < TPC) {
         const int sub = tk % LPT;
         const int t = tc0 + g;
-        float psum;
-        topk_lanes<LPT, NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum);
+        float psum, inv;
+        topk_lanes<LPT, NV>(s_logit + g * e_pad, p.E, p.topk, sub, s_ids + g * 32, s_p + g * 32, psum, inv);
         __syncwarp();
         if (t < p.T) {
           for (int r = sub; r < p.topk; r += LPT) {
             p.ids[static_cast<size_t>(t) * p.topk + r] = s_ids[g * 32 + r];
-            p.w[static_cast<size_t>(t) * p.topk + r] = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r];
+            p.w[static_cast<size_t>(t) * p.topk + r] = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r] * inv;
           }
         }
       }

@@ -90,6 +90,22 @@ def test_gpt_oss_shaped_layer(cuda, T):
     check_layer(GPT_OSS_20B, T, 71, cuda)
 
 
+def test_batch_invariance_across_kernels(cuda):
+    """A token's output does not depend on the batch it rides in: decode-size batches (tiny
+    kernel), memory-bound batches (k_experts) and compute-bound ones (CTA-pair kernel) give
+    bit-identical rows (routing sums K in a fixed order; every kernel accumulates each output
+    element over K in the same order)."""
+    s = QWEN3_30B_A3B
+    layer = make(s, 95, cuda)[3]
+    x = router_tokens(4100, s.hidden, 96).to(cuda)
+    y_big, _ = layer(x)
+    y_mid, _ = layer(x[:576].contiguous())
+    y_one, _ = layer(x[7:8].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(y_mid, y_big[:576])
+    assert torch.equal(y_one[0], y_big[7])
+
+
 def test_max_experts_large_batch(cuda):
     """E = 256 (two router m-tiles) at a batch large enough for 64-token router tiles: the router
     must keep 16-token tiles there (a 64-token ring would need 247 KB of shared memory)."""
@@ -249,7 +265,7 @@ def test_host_pipeline_matches_device_forward(cuda):
 
 
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
-                                  "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1"])
+                                  "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
