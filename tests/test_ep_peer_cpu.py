@@ -1,0 +1,96 @@
+"""Peer-memory EP protocol on the CPU: world size 2 over gloo, shared-memory CPU tensors as
+the peer buffers, the fp32 oracle as the compute (oracle/ep_peer.py restates ep_p2p.cuh).
+
+Checks the layout math of the fused path (counts inbox, per-(owner, expert) row bases,
+expert-major/source-major receive order, owner expert offsets, return addressing): every
+rank's output equals the single-device oracle layer on its own tokens. The GPU kernels are
+checked against the single-GPU layer bit for bit in tests/test_gpu_ep_p2p.py.
+"""
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import ep_peer
+from oracle import moe_oracle as mo
+from paper_2510_08055_b200.types import MoEShape
+
+SHAPE = MoEShape(hidden=256, ffn=128, num_experts=16, top_k=4, norm_topk_prob=True)
+
+
+def _weights(skew=False):
+    from paper_2510_08055_b200.synthetic import expert_weights, router_weight
+
+    wr = router_weight(SHAPE.num_experts, SHAPE.hidden, 5).float()
+    if skew:
+        wr[:4, SHAPE.hidden - 1] = 16.0
+    w13, w2 = expert_weights(SHAPE.num_experts, SHAPE.hidden, SHAPE.ffn, 6)
+    return wr.numpy(), w13.float().numpy(), w2.float().numpy()
+
+
+def _worker(rank, world, port, tokens, skew, bufs, q):
+    from paper_2510_08055_b200.synthetic import router_tokens
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        inbox, recv, y_out = bufs
+        P, E, k = world, SHAPE.num_experts, SHAPE.top_k
+        El = E // P
+        wr, w13, w2 = _weights(skew)
+        x = router_tokens(tokens[rank], SHAPE.hidden, 40 + rank).float().numpy()
+        ids, w, _ = mo.route(x, wr, k, SHAPE.norm_topk_prob)
+        counts, offsets, slot_of, _ = mo.permute(ids, E)
+        ep_peer.post_counts(counts, [b.numpy() for b in inbox], P, El, rank)
+        dist.barrier()
+        dest_base, off_local = ep_peer.plan([b.numpy() for b in inbox], P, El, rank)
+        dest_rank, dest_row = ep_peer.dispatch(x, ids, slot_of, offsets, dest_base, [b.numpy() for b in recv], El)
+        dist.barrier()
+        R = int(off_local[El])
+        _, yl = mo.experts(recv[rank].numpy()[:R], off_local, w13[rank * El:(rank + 1) * El],
+                           w2[rank * El:(rank + 1) * El])
+        y_out[rank].numpy()[:R] = yl
+        dist.barrier()
+        y = ep_peer.combine([b.numpy() for b in y_out], dest_rank, dest_row, w)
+        ref = mo.moe_forward(x, wr, w13, w2, k, SHAPE.norm_topk_prob)["y"]
+        ok = np.allclose(y, ref, rtol=1e-5, atol=1e-6) and R == int(np.asarray(inbox[rank]).sum())
+        dist.barrier()
+        q.put((rank, bool(ok), float(np.abs(y - ref).max()) if y.size else 0.0))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(tokens, skew=False, world=2):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cap = sum(tokens) * SHAPE.top_k
+    El = SHAPE.num_experts // world
+    bufs = ([torch.zeros(world * El, dtype=torch.int64).share_memory_() for _ in range(world)],
+            [torch.zeros((max(cap, 1), SHAPE.hidden), dtype=torch.float32).share_memory_() for _ in range(world)],
+            [torch.zeros((max(cap, 1), SHAPE.hidden), dtype=torch.float32).share_memory_() for _ in range(world)])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, tokens, skew, bufs, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, ok, err = q.get(timeout=300)
+        res[r] = (ok, err)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r][0], f"rank {r}: max abs err {res[r][1]}"
+
+
+def test_peer_protocol_balanced():
+    _run([40, 24])
+
+
+def test_peer_protocol_skewed_and_empty_rank():
+    _run([30, 0], skew=True)
