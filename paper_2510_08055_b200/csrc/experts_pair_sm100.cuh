@@ -359,18 +359,19 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       aph ^= 1;
       tc_fence_after();
       const uint32_t t0 = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
-      const int nchunks = (nvalid + 15) / 16;
+      // 32-column TMEM loads: one wait per 32 tokens (the drain is on the MMA's critical path)
+      const int nchunks32 = (nvalid + 31) / 32;
       if (kind == kItemUp) {
         const int feat = m0 + static_cast<int>(rank) * C::kUpFeat + 32 * q + lane;
         __nv_bfloat16* dst = p.act + static_cast<size_t>(row0) * p.I + feat;
-        for (int c = half; c < nchunks; c += 2) {
-          uint32_t g[16], u[16];
-          tmem_ld16(t0 + c * 16, g);
-          tmem_ld16(t0 + C::kN + c * 16, u);
+        for (int c = half; c < nchunks32; c += 2) {
+          uint32_t g[32], u[32];
+          tmem_ld32(t0 + c * 32, g);
+          tmem_ld32(t0 + C::kN + c * 32, u);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = c * 16 + i;
+          for (int i = 0; i < 32; ++i) {
+            const int n = c * 32 + i;
             if (n < nvalid)
               dst[static_cast<size_t>(n) * p.I] =
                   __float2bfloat16_rn(silu_mul(__uint_as_float(g[i]), __uint_as_float(u[i])));
@@ -379,14 +380,14 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       } else {
         const int feat = m0 + static_cast<int>(rank) * C::kDnRows + 32 * q + lane;
         __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
-        for (int c = half; c < nchunks; c += 2) {
-          uint32_t v[16], v2[16];
-          tmem_ld16(t0 + c * 16, v);
-          tmem_ld16(t0 + C::kN + c * 16, v2);
+        for (int c = half; c < nchunks32; c += 2) {
+          uint32_t v[32], v2[32];
+          tmem_ld32(t0 + c * 32, v);
+          tmem_ld32(t0 + C::kN + c * 32, v2);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = c * 16 + i;
+          for (int i = 0; i < 32; ++i) {
+            const int n = c * 32 + i;
             if (n < nvalid) {
               dst[static_cast<size_t>(n) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
               dst[static_cast<size_t>(n) * p.H + kTileM] = __float2bfloat16_rn(__uint_as_float(v2[i]));
