@@ -51,13 +51,18 @@ namespace lp {
 #define PW_CLUSTER(bar, par, tag) mbar_wait_cluster((bar), (par))
 #endif
 
+// BN: token-tile width. 256: one item's two accumulators fill TMEM (single-
+// buffered); 128: two items' accumulators fit, so the drain overlaps the next
+// item's MMAs at the price of more operand bytes per MAC.
+template <int BN>
 struct PairCfg {
-  static constexpr int kN = 256;                      // tokens per item (MMA N)
+  static constexpr int kN = BN;                       // tokens per item (MMA N)
   static constexpr int kBRows = kN / 2;               // B rows staged per CTA
   static constexpr int kStageBytes = 2 * kATileBytes + kBRows * 128;
-  static constexpr int kStages = 4;
-  static constexpr int kTmemCols = 2 * kN;            // gate | up (single-buffered)
-  static constexpr int kAuxBytes = 8 * (3 * kStages + 2 + 2 * kRing) + 16 * kRing + 16 + 4 * (3 * kMaxExperts + 2);
+  static constexpr int kStages = BN >= 256 ? 4 : 5;
+  static constexpr int kAcc = BN >= 256 ? 1 : 2;      // accumulator sets (gate | up) in TMEM
+  static constexpr int kTmemCols = 512;
+  static constexpr int kAuxBytes = 8 * (3 * kStages + 1 + 2 * kAcc + 2 * kRing) + 16 * kRing + 16 + 4 * (3 * kMaxExperts + 2);
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
   static constexpr int kUpFeat = 128;                 // act features per CTA per UP item
   static constexpr int kDnRows = 256;                 // W2 rows per CTA per DN item
@@ -67,24 +72,25 @@ struct PairCfg {
 // cp.async by warps 2-3 of each CTA (its half of the tile), as in k_experts'
 // memory-bound path; the peer's completions are relayed to the leader's B-full
 // barrier by the peer's otherwise idle warp 1. No x_perm is materialised.
-template <bool GATHER>
+template <bool GATHER, int BN>
 __global__ void __launch_bounds__(kExpertsThreads, 1)
     k_experts_pair(const __grid_constant__ CUtensorMap tm_w13, const __grid_constant__ CUtensorMap tm_w2,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_act,
                    const ExpertsParams p) {
-  using C = PairCfg;
+  using C = PairCfg<BN>;
   constexpr int S_ = C::kStages;
+  constexpr int A_ = C::kAcc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* aux = smem + S_ * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);  // leader's counts both CTAs' bytes
   uint64_t* empty = full + S_;
-  uint64_t* tfull = empty + S_;
-  uint64_t* tempty = tfull + 1;                       // leader's counts both CTAs' epilogue warps
-  uint64_t* sfull = tempty + 1;
+  uint64_t* tfull = empty + S_;                       // [A_]
+  uint64_t* tempty = tfull + A_;                      // [A_] leader's counts both CTAs' epilogue warps
+  uint64_t* sfull = tempty + A_;
   uint64_t* sempty = sfull + kRing;                   // leader's counts both CTAs' consumers
   uint64_t* bfull = sempty + kRing;                   // GATHER: this CTA's B half landed (+ peer relay on the leader)
-  int4* ring = reinterpret_cast<int4*>(bfull + S_);
+  int4* ring = reinterpret_cast<int4*>(bfull + ((S_ + 1) & ~1));  // 16-byte aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   int32_t* s_off = reinterpret_cast<int32_t*>(tmem_slot + 4);
   int32_t* s_tp = s_off + (kMaxExperts + 1);
@@ -98,8 +104,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S_; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 16);  // 8 epilogue warps x 2 CTAs
+    for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 16); }  // 8 epi warps x 2 CTAs
     // ring consumers: MMA + epilogue (leader), producer + epilogue (peer); GATHER adds
     // both CTAs' two gather warps and the peer's relay
     for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], GATHER ? 9 : 4); }
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     if (leader && lane == 0) {
       int stage = 0; uint32_t phase = 0;
       int r = 0; uint32_t rph = 0;
-      uint32_t aph = 0;
+      int acc = 0; uint32_t aph = 0;
       while (true) {
         PW_LOCAL(&sfull[r], rph, "mma:sfull");
         const int4 info = ring[r];
@@ -238,9 +243,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
         const bool up = kind == kItemUp;
         const uint32_t idesc = idesc_bf16_f32(256, (info.w + 15) & ~15);
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
-        PW_CLUSTER(tempty, aph ^ 1, "mma:tempty");
+        PW_CLUSTER(&tempty[acc], aph ^ 1, "mma:tempty");
         tc_fence_after();
-        const uint32_t d0 = tmem_base, d1 = tmem_base + C::kN;
+        const uint32_t d0 = tmem_base + acc * 2 * C::kN, d1 = d0 + C::kN;
         for (int kb = 0; kb < kblocks; ++kb) {
           PW_LOCAL(&full[stage], phase, "mma:full");
           if (GATHER) PW_LOCAL(&bfull[stage], phase, "mma:bfull");
@@ -258,8 +263,8 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
           mma_commit_pair(&empty[stage]);
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
-        mma_commit_pair(tfull);
-        aph ^= 1;
+        mma_commit_pair(&tfull[acc]);
+        if (++acc == A_) { acc = 0; aph ^= 1; }
       }
     } else if (GATHER && !leader && lane == 0) {
       // relay: the peer's B half of a stage landed -> arrive on the leader's bfull
@@ -344,10 +349,10 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
     const int q = warp & 3;             // TMEM lane quarter this warp may access
     const int half = (warp - 4) >> 2;   // 0: even chunks, 1: odd chunks
     const int et = threadIdx.x - 128;   // 0..255
-    const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t sempty_leader0 = mapa_shared(smem_u32(&sempty[0]), 0);
     int r = 0; uint32_t rph = 0;
-    uint32_t aph = 0;
+    int acc = 0; uint32_t aph = 0;
     while (true) {
       if (leader) PW_LOCAL(&sfull[r], rph, "epi:sfull");
       else PW_CLUSTER(&sfull[r], rph, "peerepi:sfull");
@@ -355,10 +360,9 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       const int kind = info.x & 0xff;
       if (kind == kItemEnd) break;
       const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
-      PW_LOCAL(tfull, aph, "epi:tfull");
-      aph ^= 1;
+      PW_LOCAL(&tfull[acc], aph, "epi:tfull");
       tc_fence_after();
-      const uint32_t t0 = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+      const uint32_t t0 = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * 2 * C::kN;
       // 32-column TMEM loads: one wait per 32 tokens (the drain is on the MMA's critical path)
       const int nchunks32 = (nvalid + 31) / 32;
       if (kind == kItemUp) {
@@ -398,9 +402,10 @@ __global__ void __launch_bounds__(kExpertsThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (leader) mbar_arrive(tempty);
-        else mbar_arrive_remote(tempty_leader);
+        if (leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_remote(tempty_leader0 + acc * 8);
       }
+      if (++acc == A_) { acc = 0; aph ^= 1; }
       if (kind == kItemUp) {
         fence_proxy_async_global();       // act rows are read back through TMA (async proxy)
         named_bar_sync(1, kEpiThreads);   // every thread's act stores precede the count

@@ -74,13 +74,20 @@ bool use_pdl() {
   return v;
 }
 
+// Token-tile width of the CTA-pair kernel in the compute-bound regime
+// (LPMOE_PAIR_N: 256 default; 128 double-buffers the accumulator).
+int pair_n() {
+  static const int v = env_int("LPMOE_PAIR_N", 256);
+  return v == 128 ? 128 : 256;
+}
+
 int pick_max_n(int S, int E) {
   static const int forced = env_int("LPMOE_MAX_N", 0);
   if (forced == 64 || forced == 128 || forced == 256) return forced;
   const int avg = (S + E - 1) / E;
   if (avg <= 40) return 64;
   if (avg <= 96) return 128;
-  return 256;
+  return pair_n();
 }
 
 // Workspace header (fixed offsets, independent of T): router tickets and the
@@ -408,10 +415,10 @@ int launch_experts_t(const void* src, int src_rows, const void* act_in, int S, c
 // (cta_group::2, experts_pair_sm100.cuh). LPMOE_PAIR=0 selects k_experts<256>.
 bool use_pair(int max_n, int H, int I) {
   static const int v = env_int("LPMOE_PAIR", 1);
-  return v != 0 && max_n == 256 && H % 512 == 0 && I % 256 == 0;
+  return v != 0 && (max_n == 256 || (max_n == 128 && pair_n() == 128)) && H % 512 == 0 && I % 256 == 0;
 }
 
-template <bool GATHER>
+template <bool GATHER, int BN>
 int launch_experts_pair(const void* src, int src_rows, int S, const void* act, const void* w13, const void* w2, int H,
                         int I, int E, const lp::ExpertsParams& p, cudaStream_t st) {
   int rc;
@@ -421,8 +428,8 @@ int launch_experts_pair(const void* src, int src_rows, int S, const void* act, c
   if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
   if ((rc = make_tmap(&tm_x, src, src_rows, H, lp::kBoxRows))) return rc;
   if ((rc = make_tmap(&tm_act, act, S, I, lp::kBoxRows))) return rc;
-  constexpr int smem = lp::PairCfg::kSmemBytes;
-  if ((rc = set_smem(lp::k_experts_pair<GATHER>, smem))) return rc;
+  constexpr int smem = lp::PairCfg<BN>::kSmemBytes;
+  if ((rc = set_smem(lp::k_experts_pair<GATHER, BN>, smem))) return rc;
   const int sms = sm_count();
   static int max_clusters = -1;  // pairs that fit at once (one CTA per SM)
   if (max_clusters < 0) {
@@ -438,13 +445,13 @@ int launch_experts_pair(const void* src, int src_rows, int S, const void* act, c
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, lp::k_experts_pair<GATHER>, &cfg) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&n, lp::k_experts_pair<GATHER, BN>, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = sms / 2;
     }
     max_clusters = n < sms / 2 ? n : sms / 2;
   }
-  LP_CUDA(launch_pdl_cluster(lp::k_experts_pair<GATHER>, 2 * max_clusters, lp::kExpertsThreads, smem, st, 2, tm_w13, tm_w2,
+  LP_CUDA(launch_pdl_cluster(lp::k_experts_pair<GATHER, BN>, 2 * max_clusters, lp::kExpertsThreads, smem, st, 2, tm_w13, tm_w2,
                              tm_x, tm_act, p));
   return LP_OK;
 }
@@ -541,9 +548,10 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
   if (fc.y == nullptr && use_pair(max_n, H, I)) {
     if (tok_of) {  // rows gathered by the kernel's cp.async warps from the unpermuted source
       p.xsrc = static_cast<const __nv_bfloat16*>(src);
-      return launch_experts_pair<true>(src, src_rows, S, act, w13, w2, H, I, E, p, st);
+      return launch_experts_pair<true, 256>(src, src_rows, S, act, w13, w2, H, I, E, p, st);
     }
-    return launch_experts_pair<false>(src, S, S, act, w13, w2, H, I, E, p, st);
+    if (max_n == 128) return launch_experts_pair<false, 128>(src, S, S, act, w13, w2, H, I, E, p, st);
+    return launch_experts_pair<false, 256>(src, S, S, act, w13, w2, H, I, E, p, st);
   }
   if (tok_of) {  // rows gathered by the kernel's cp.async warps from the unpermuted source
     p.xsrc = static_cast<const __nv_bfloat16*>(src);
