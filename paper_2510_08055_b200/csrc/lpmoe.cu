@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <utility>
 
@@ -198,8 +199,45 @@ int get_encode() {
   return LP_OK;
 }
 
+// Encoded descriptors are a pure function of (address, shape, box): cache them,
+// encoding is host time on every layer call otherwise (weights never move;
+// activation buffers recur through the caching allocator). Bounded: cleared when full.
+struct TmapKey {
+  const void* ptr;
+  uint64_t rows, cols;
+  uint32_t box_rows;
+  bool operator<(const TmapKey& o) const {
+    if (ptr != o.ptr) return ptr < o.ptr;
+    if (rows != o.rows) return rows < o.rows;
+    if (cols != o.cols) return cols < o.cols;
+    return box_rows < o.box_rows;
+  }
+};
+std::mutex g_tmap_mu;
+std::map<TmapKey, CUtensorMap> g_tmap_cache;
+
+int encode_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
 // bf16 matrix [rows, cols] row-major, box = 64 cols (128 B, SWIZZLE_128B) x box_rows.
 int make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  const TmapKey key{ptr, rows, cols, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    auto it = g_tmap_cache.find(key);
+    if (it != g_tmap_cache.end()) {
+      *m = it->second;
+      return LP_OK;
+    }
+  }
+  int rc = encode_tmap(m, ptr, rows, cols, box_rows);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  if (g_tmap_cache.size() >= 4096) g_tmap_cache.clear();
+  g_tmap_cache.emplace(key, *m);
+  return LP_OK;
+}
+
+int encode_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
@@ -258,10 +296,26 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return launch_pdl_cluster(kernel, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
+// Dynamic shared-memory opt-in, set once per (kernel, device, size): the
+// attribute call is host overhead on every layer of a decode step otherwise.
+std::mutex g_smem_mu;
+std::map<std::pair<const void*, int>, int> g_smem_set;
+
 template <typename K>
 int set_smem(K kernel, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  {
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    auto it = g_smem_set.find(key);
+    if (it != g_smem_set.end() && it->second >= bytes) return LP_OK;
+  }
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return fail(LP_ECUDA, "cudaFuncSetAttribute(smem=%d): %s", bytes, cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  int& v = g_smem_set[key];
+  if (bytes > v) v = bytes;
   return LP_OK;
 }
 

@@ -32,10 +32,90 @@ from .synthetic import router_weight
 from .types import ModelSpec, MoEShape
 
 
+class _DecodeGraphs:
+    """CUDA graphs of single decode-size layer steps (T <= max_tokens rows): a step is
+    `add_rmsnorm(x, y_prev, xn); layer(xn) -> y, counts`, captured once per (T, layer,
+    first?) on static buffers and replayed. Decode layers move a few hundred MB in
+    ~40 us, which the per-call host cost (Python + ctypes + 5 launches, ~40 us)
+    would otherwise match: replay keeps a decode step device-bound. The captured
+    layers run on their own small workspace (the shared one grows for prefill
+    batches, which would move its address under a captured graph)."""
+
+    def __init__(self, model: "MoEModel", max_tokens: int):
+        self.model, self.max_tokens = model, max_tokens
+        dev, s = model.device, model.shape
+        self.workspace = Workspace(dev)
+        self.layers = [GpuMoE(s, m.wr, m.w13, m.w2, workspace=self.workspace) for m in model.layers]
+        # fixed size (the largest any T <= max_tokens asks for): never regrows under a graph
+        self.workspace.get(max(self.layers[0].workspace_bytes(t) for t in range(1, max_tokens + 1)))
+        for layer in self.layers:
+            layer._bufs(max_tokens)
+        self.pool = torch.cuda.graph_pool_handle()
+        self.bufs: dict[int, tuple] = {}
+        self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+
+    def _buffers(self, T: int):
+        b = self.bufs.get(T)
+        if b is None:
+            dev, s = self.model.device, self.model.shape
+            b = (torch.zeros((T, s.hidden), dtype=torch.bfloat16, device=dev),   # x (residual, in place)
+                 torch.zeros((T, s.hidden), dtype=torch.bfloat16, device=dev),   # xn
+                 torch.zeros((T, s.hidden), dtype=torch.bfloat16, device=dev),   # y
+                 torch.zeros((self.model.num_layers, s.num_experts), dtype=torch.int32, device=dev))  # counts
+            self.bufs[T] = b
+        return b
+
+    def _graph(self, T: int, layer: int, first: bool) -> torch.cuda.CUDAGraph:
+        key = (T, layer, first)
+        g = self.graphs.get(key)
+        if g is None:
+            x, xn, y, c = self._buffers(T)
+            step = lambda: (add_rmsnorm(x, None if first else y, xn),  # noqa: E731
+                            self.layers[layer](xn, out=y, counts_out=c[layer]))
+            dev = self.model.device
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            saved = x.clone(), y.clone()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                step()  # warm-up outside the capture (kernel attributes, descriptors)
+                # capture_begin/end directly: the torch.cuda.graph context's gc.collect() and
+                # empty_cache() per capture would dominate capturing hundreds of small graphs
+                g.capture_begin(pool=self.pool)
+                step()
+                g.capture_end()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            x.copy_(saved[0])
+            y.copy_(saved[1])
+            self.graphs[key] = g
+        return g
+
+    def capture(self, token_counts) -> None:
+        """Capture every layer step for these batch sizes up front (outside timed iterations)."""
+        for T in token_counts:
+            if 0 < T <= self.max_tokens:
+                for layer in range(self.model.num_layers):
+                    for first in (True, False):
+                        self._graph(T, layer, first)
+        torch.cuda.synchronize(self.model.device)
+
+    def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor) -> torch.Tensor:
+        T = x.shape[0]
+        sx, sxn, sy, sc = self._buffers(T)
+        sx.copy_(x)
+        for i, layer in enumerate(range(l0, l1)):
+            self._graph(T, layer, i == 0).replay()
+        counts[l0:l1] += sc[l0:l1]
+        add_rmsnorm(sx, sy, sxn)
+        x.copy_(sx)
+        return x
+
+
 class MoEModel:
     """`num_layers` resident MoE layers of `shape` with random-init weights."""
 
-    def __init__(self, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0, std: float = 0.02):
+    def __init__(self, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0, std: float = 0.02,
+                 graph_tokens: int = 0):
         self.shape, self.num_layers = shape, num_layers
         self.device = torch.device(device)
         self.layers: list[GpuMoE] = []
@@ -47,11 +127,15 @@ class MoEModel:
             w2 = (torch.randn((E, H, I), generator=g, device=self.device) * std).to(torch.bfloat16)
             wr = router_weight(E, H, seed * 1000 + i).to(self.device)
             self.layers.append(GpuMoE(shape, wr, w13, w2, workspace=self.workspace))
+        # decode-size segments (T <= graph_tokens) replay per-layer CUDA graphs
+        self.graphs = _DecodeGraphs(self, graph_tokens) if graph_tokens > 0 else None
 
     def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor) -> torch.Tensor:
         """h <- h + MoE_l(RMSNorm(h)) for l in [l0, l1) (Qwen3's pre-MoE norm keeps the
         residual stream bounded); per-expert counts of layer l are added into counts[l]."""
         T = x.shape[0]
+        if self.graphs is not None and 0 < T <= self.graphs.max_tokens:
+            return self.graphs.run_segment(x, l0, l1, counts)
         xn = torch.empty_like(x)
         y = torch.empty_like(x)
         c = torch.empty((l1 - l0, self.shape.num_experts), dtype=torch.int32, device=self.device)
@@ -74,6 +158,7 @@ class MeasuredCost:
         self.spec, self.stack = model_spec, stack
         self.keep_final_prompt = keep_final_prompt
         self.final_prompt: dict[int, torch.Tensor] = {}
+        self.final_decode: dict[int, torch.Tensor] = {}  # last decode hidden row of finished requests
         self.dev = stack.device
         self.H = stack.shape.hidden
         self.stash: dict[int, torch.Tensor] = {}    # rid -> [input_len, H] prompt activations
@@ -158,5 +243,7 @@ class MeasuredCost:
         # drop finished requests' state
         live = {r.id for r in st.decoding} | set(plan.decode_ids)
         for rid in [k for k in self.decode_row if k not in live]:
-            del self.decode_row[rid]
+            row = self.decode_row.pop(rid)
+            if self.keep_final_prompt:
+                self.final_decode[rid] = row
         return ks

@@ -57,3 +57,25 @@ def test_measured_iterations_follow_the_modelled_plan(stack):
         for n, h in zip(log["routed"], log["experts_hit"]):
             assert (h == 0) == (n == 0) and h <= 16 and (n == 0 or h >= 2)
         assert rec.expert_load_bytes == sum(log["experts_hit"]) * TINY_MODEL.bytes_per_expert
+
+
+def test_decode_graphs_match_eager(cuda):
+    """Per-layer CUDA graphs for decode-size segments (MoEModel(graph_tokens=...)) give the
+    same hidden states, routing and expert bytes as eager calls."""
+    # all arrivals at t=0: the plan stream cannot depend on the measured (graph vs eager) timings
+    reqs = [sv.Request(i, 0.0, n, 7) for i, n in enumerate((700, 40, 300, 5))]
+    eager = MoEModel(TINY, 4, device=cuda, seed=3)
+    graphed = MoEModel(TINY, 4, device=cuda, seed=3, graph_tokens=16)
+    res = []
+    for stack in (eager, graphed):
+        cost = MeasuredCost(TINY_MODEL, stack, keep_final_prompt=True)
+        recs, done, _ = sv.run(TINY_MODEL, cm.B200_MODELLED, sv.Planner("layered", 512, 512), reqs, cost)
+        res.append((recs, cost))
+    (ra, ca), (rb, cb) = res
+    assert len(graphed.graphs.graphs) > 0
+    assert [r.expert_load_bytes for r in ra] == [r.expert_load_bytes for r in rb]
+    assert [g["experts_hit"] for g in ca.iter_log] == [g["experts_hit"] for g in cb.iter_log]
+    for rid in range(4):
+        assert torch.equal(ca.final_prompt[rid], cb.final_prompt[rid]), rid
+        last = [c.final_decode.get(rid, c.decode_row.get(rid)) for c in (ca, cb)]  # finished / still live
+        assert last[0] is not None and torch.equal(last[0], last[1]), rid

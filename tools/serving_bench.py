@@ -63,6 +63,8 @@ def main():
     ap.add_argument("--config", choices=["c3", "c4", "c5"], default="c3")
     ap.add_argument("--requests", type=int, default=100)
     ap.add_argument("--prompt", type=int, default=8192)
+    ap.add_argument("--graph-tokens", type=int, default=0,
+                    help="capture per-layer CUDA graphs for decode segments up to this many rows (0: eager)")
     ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (workload.export_trace) instead of "
                                                  "the committed arXiv request fixture")
     a = ap.parse_args()
@@ -70,8 +72,12 @@ def main():
     from paper_2510_08055_b200.executor import MoEModel
 
     t0 = time.time()
-    stack = MoEModel(QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL.num_layers, device="cuda", seed=11)
-    print(json.dumps({"setup": "48 resident layers", "seconds": time.time() - t0}), flush=True)
+    stack = MoEModel(QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL.num_layers, device="cuda", seed=11,
+                     graph_tokens=a.graph_tokens)
+    if stack.graphs is not None:  # decode-only layer steps replay CUDA graphs (captured up front)
+        stack.graphs.capture(range(1, a.graph_tokens + 1))
+    print(json.dumps({"setup": "48 resident layers", "seconds": time.time() - t0,
+                      "decode_graph_tokens": a.graph_tokens}), flush=True)
     L = a.prompt
     if a.config == "c3":
         reqs = [sv.Request(i, 0.0, 128, 256) for i in range(32)] + [sv.Request(32, 0.0005, L, 16)]
