@@ -442,7 +442,7 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
                        tok_of));
     return LP_OK;
   }
-  LP_CUDA(launch_pdl(lp::k_scatter, (S + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
+  LP_CUDA(launch_pdl(lp::k_scatter, (T + 7) / 8, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist), rank_local,
                      static_cast<const int32_t*>(offsets), static_cast<const __nv_bfloat16*>(x), S, E, topk, H,
                      chunk_tokens * topk, slot_of, tok_of, static_cast<__nv_bfloat16*>(x_perm)));
   return LP_OK;

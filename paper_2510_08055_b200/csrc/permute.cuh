@@ -169,8 +169,9 @@ __global__ void __launch_bounds__(kScanThreads)
   if (tid == 0) LP_TRACE_AT(true, 18);
 }
 
-// One warp per routing entry i = t*topk + j: its expert-contiguous slot, the
-// inverse map, and (optionally) the copy of token row t into x_perm[slot].
+// One warp per token t: lane j < topk computes the expert-contiguous slot of
+// routing entry t*topk + j and the inverse map; the warp then reads token row
+// t once (8 x 16 B per lane in flight) and writes it to its topk slots of x_perm.
 __global__ void __launch_bounds__(256)
     k_scatter(const int32_t* __restrict__ ids, const int32_t* __restrict__ chunk_base,
               const int32_t* __restrict__ rank_local, const int32_t* __restrict__ offsets,
@@ -178,23 +179,34 @@ __global__ void __launch_bounds__(256)
               int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of, __nv_bfloat16* __restrict__ x_perm) {
   pdl_trigger();
   pdl_wait();
-  const int i = blockIdx.x * 8 + threadIdx.x / 32;
+  const int t = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) LP_TRACE_MIN(24);
-  if (i >= S) return;
-  const int e = __ldcg(ids + i);
-  const int t = i / topk;
-  const int slot = __ldcg(offsets + e) + __ldcg(chunk_base + static_cast<size_t>(i / chunk) * E + e) +
-                   __ldcg(rank_local + i);
-  if (lane == 0) {
+  if (t * topk >= S) return;
+  int slot = 0;
+  if (lane < topk) {
+    const int i = t * topk + lane;
+    const int e = __ldcg(ids + i);
+    slot = __ldcg(offsets + e) + __ldcg(chunk_base + static_cast<size_t>(i / chunk) * E + e) + __ldcg(rank_local + i);
     slot_of[i] = slot;
     tok_of[slot] = t;
   }
   if (x_perm != nullptr) {
     const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
-    uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(slot) * H);
     const int nv = H / 8;
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+    for (int v0 = 0; v0 < nv; v0 += 8 * 32) {
+      uint4 r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (v0 + u * 32 + lane < nv) r[u] = __ldg(src + v0 + u * 32 + lane);
+      for (int j = 0; j < topk; ++j) {
+        const int sj = __shfl_sync(0xffffffffu, slot, j);
+        uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(sj) * H);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (v0 + u * 32 + lane < nv) dst[v0 + u * 32 + lane] = r[u];
+      }
+    }
   }
   if (lane == 0) LP_TRACE_MAX(25);
 }
