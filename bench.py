@@ -299,10 +299,12 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     # timed region: plain back-to-back steps (stage events would split the PDL chain)
     t_region0 = time.monotonic()
+    n_launch0 = lib.lp_launch_count()
     start.record(stream)
     for i in range(K):
         step(i)
     end.record(stream)
+    n_launches = lib.lp_launch_count() - n_launch0
     torch.cuda.synchronize()
     t_region1 = time.monotonic()
     clocks.stop()
@@ -394,12 +396,11 @@ def run_ours(args, rank: int, world: int):
                          f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                 "d2h_bytes_per_step": T * s.hidden * 2},
-        # ours per step: fused path = router, scan, scatter, experts, combine; EP adds the
-        # standalone permutes (3 each), the expert-plan kernel and a second combine
-        # ours per step: fused layer 5 (router, scan, slots/scatter, experts, combine); NCCL EP 11 (+NCCL's);
-        # peer-memory EP 14 (route, chunk_hist, scan, slots, post_counts, plan, dispatch, k_plan, experts,
-        # combine, 4 barriers)
-        "gpu_launches": (5 if world == 1 else (14 if args.ep == "p2p" else 11)) * K,
+        # our kernels launched inside the timed region, counted by liblpmoe (lp_launch_count):
+        # single GPU 4 per step (router, scan+slots, experts, combine) in the gather regime,
+        # 5 with x_perm (router, scan, scatter, experts, combine); EP adds its plan/dispatch/
+        # combine kernels and barriers (NCCL's own kernels are not counted)
+        "gpu_launches": n_launches,
         "clocks": clocks.summary(t_region0, t_region1),
     }
     if stage_us is not None:

@@ -46,6 +46,11 @@ const char* lp_version(void);
  * returns the last error code. */
 int lp_last_error(char* buf, size_t n);
 
+/* Number of kernels this library has launched in the process so far (all
+ * entry points, all threads). Not a reference interface: host-side evidence
+ * of which native kernels ran inside a timed region (bench.py gpu_launches). */
+uint64_t lp_launch_count(void);
+
 /* Bytes of scratch `lp_moe_forward` needs for this shape (>= 0, 256-aligned
  * regions). Also sufficient for every staged call below. The workspace must be
  * zero-filled ONCE after allocation (its fixed-offset header holds the

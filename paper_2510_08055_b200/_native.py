@@ -30,6 +30,7 @@ _sz = ctypes.c_size_t
 SIGNATURES = {
     "lp_version": (ctypes.c_char_p, []),
     "lp_last_error": (_i, [ctypes.c_char_p, _sz]),
+    "lp_launch_count": (ctypes.c_uint64, []),
     "lp_moe_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "lp_moe_route": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _sz, _p]),
     "lp_moe_permute": (_i, [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _sz, _p]),

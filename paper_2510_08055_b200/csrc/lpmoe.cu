@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <utility>
 
@@ -264,6 +265,11 @@ int sm_count() {
   return n;
 }
 
+// Kernels this library has launched (lp_launch_count): host-side evidence of
+// which native kernels ran inside a timed region.
+std::atomic<unsigned long long> g_launches{0};
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its stream predecessor drains; kernels pdl_wait() before global I/O.
 template <typename... KArgs, typename... Args>
@@ -287,6 +293,7 @@ cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -418,6 +425,13 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   return launch_router_dispatch<false>(tm_wr, tm_x, rp, ntiles, TN, L.csize, e_pad, st);
 }
 
+// Scan and slot maps fused into one launch when no x_perm is materialised
+// (LPMOE_SCAN_SLOTS=0: the two-kernel k_scan + k_slots path).
+bool use_scan_slots() {
+  static const bool v = env_int("LPMOE_SCAN_SLOTS", 1) != 0;
+  return v;
+}
+
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
 // Scan (one CTA): per-tile bases, counts, offsets, expert tile schedule. Scatter
 // (one warp per routing entry): slot_of / tok_of and, if x_perm, the row copy.
@@ -428,6 +442,13 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
                         int zero_n = 0) {
   const int S = T * topk;
   const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
+  const int chunk = chunk_tokens * topk;
+  if (x_perm == nullptr && zero_n == 0 && use_scan_slots() && S > 0 && 256 / chunk + 2 <= lp::kScanSlotsTiles) {
+    LP_CUDA(launch_pdl(lp::k_scan_slots, (S + 255) / 256, 256, 0, st, static_cast<const int32_t*>(chunk_hist), nchunks,
+                       ids, rank_local, S, E, topk, chunk, max_n, counts, offsets, tile_prefix, tile_rows, sched,
+                       slot_of, tok_of));
+    return LP_OK;
+  }
   const int n_hist = nchunks * E;
   const int smem = n_hist <= lp::kScanSmemInts ? n_hist * 4 : 0;
   if (smem > 48 * 1024) {
@@ -652,6 +673,8 @@ __global__ void k_plan(const int32_t* __restrict__ offsets, int E, int max_n, in
 // ====================================================================== C ABI
 extern "C" {
 
+uint64_t lp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 const char* lp_version(void) { return "lpmoe 0.1 sm_100a"; }
 
 int lp_last_error(char* buf, size_t n) {
@@ -699,6 +722,7 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   int32_t* chunk_hist = at<int32_t>(ws, L.chunk_hist);
   int32_t* rank_local = at<int32_t>(ws, L.rank_local);
   const int chunk = L.chunk_tokens * topk;
+  count_launch();
   lp::k_chunk_hist<<<(L.nchunks + lp::kHistWarps - 1) / lp::kHistWarps, 32 * lp::kHistWarps,
                      lp::kHistWarps * E * sizeof(int32_t), st>>>(ids, T * topk, E, chunk, chunk_hist, rank_local);
   LP_CHECK_LAUNCH("k_chunk_hist");
@@ -730,6 +754,7 @@ int lp_moe_experts_rows(const void* x_perm, const int32_t* offsets, int S, int S
   uint32_t* sched = at<uint32_t>(ws, kSchedOff);
   const int max_n = pick_max_n(S_hint > 0 ? S_hint : S, E);
   const int sb = (E + 31) / 32 * 32;
+  count_launch();
   k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
   LP_CHECK_LAUNCH("k_plan");
   if ((rc = launch_experts(x_perm, S, nullptr, S, w13, w2, H, I, E, max_n, offsets, tile_prefix, tile_rows, sched,
@@ -831,6 +856,7 @@ int lp_union_counts_uniform(const double* u, int trials, int batch, int k, int E
   if (!out || (batch > 0 && !u)) return fail(LP_EINVAL, "lp_union_counts_uniform: null pointer argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t sm = ((E + 31) / 32) * sizeof(uint32_t);
+  count_launch();
   if (k <= 16)
     lp::k_union_uniform<16><<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, out);
   else
@@ -847,6 +873,7 @@ int lp_union_counts_weighted(const double* u, int trials, int batch, int k, int 
   if (!out || !weights || (batch > 0 && !u)) return fail(LP_EINVAL, "lp_union_counts_weighted: null pointer argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t sm = E * sizeof(double) + ((E + 31) / 32) * sizeof(uint32_t);
+  count_launch();
   lp::k_union_weighted<<<trials, lp::kUnionThreads, sm, st>>>(u, batch, k, E, weights, out);
   LP_CHECK_LAUNCH("k_union_weighted");
   return ok();
@@ -928,6 +955,7 @@ int lp_ipc_close(void* dptr) {
 
 int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, void* stream) {
   if (P < 1 || rank < 0 || rank >= P || !peer_flag) return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
+  count_launch();
   lp::k_ep_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(peer_flag, P, rank, target);
   LP_CHECK_LAUNCH("k_ep_barrier");
   return ok();
@@ -936,6 +964,7 @@ int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, 
 int lp_ep_post_counts(const int32_t* counts, int32_t* const* peer_inbox, int P, int El, int rank, void* stream) {
   if (P < 1 || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !counts || !peer_inbox)
     return fail(LP_EINVAL, "lp_ep_post_counts: bad arguments P=%d El=%d rank=%d", P, El, rank);
+  count_launch();
   lp::k_ep_post_counts<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(counts, peer_inbox, P, El, rank);
   LP_CHECK_LAUNCH("k_ep_post_counts");
   return ok();
@@ -948,6 +977,7 @@ int lp_ep_plan(int32_t* const* peer_inbox, int P, int El, int rank, int32_t* des
     return fail(LP_EINVAL, "lp_ep_plan: bad arguments P=%d El=%d rank=%d", P, El, rank);
   const size_t sm = static_cast<size_t>(P) * P * El * sizeof(int32_t);
   if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_plan: P*P*El too large");
+  count_launch();
   lp::k_ep_plan<<<1, 256, sm, static_cast<cudaStream_t>(stream)>>>(peer_inbox, P, El, rank, dest_base, off_local);
   LP_CHECK_LAUNCH("k_ep_plan");
   return ok();
@@ -961,6 +991,7 @@ int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, co
   if (!x || !ids || !slot_of || !offsets || !dest_base || !peer_recv || !dest_rank || !dest_row)
     return fail(LP_EINVAL, "lp_ep_dispatch: null pointer argument");
   const int S = T * topk;
+  count_launch();
   lp::k_ep_dispatch<<<(S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), ids, slot_of, offsets, dest_base,
       reinterpret_cast<__nv_bfloat16* const*>(peer_recv), S, H, topk, El, dest_rank, dest_row);
@@ -973,6 +1004,7 @@ int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* 
   if (T < 0 || H <= 0 || H % 8 || topk < 1 || topk > 32) return fail(LP_EINVAL, "lp_ep_combine: bad shape");
   if (T == 0) return ok();
   if (!peer_y || !dest_rank || !dest_row || !w || !y) return fail(LP_EINVAL, "lp_ep_combine: null pointer argument");
+  count_launch();
   lp::k_ep_combine<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,
       static_cast<__nv_bfloat16*>(y));

@@ -230,6 +230,101 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) LP_TRACE_MAX(25);
 }
 
+// Scan + slot maps in one launch (gather path: no x_perm). Every CTA owns 256
+// routing entries and recomputes, from the router's per-tile histograms, what
+// it needs: per-expert totals -> offsets, and the exclusive bases of the <=
+// kScanSlotsTiles tiles its entries fall in (integer sums: identical to k_scan
+// + k_slots). CTA 0 also publishes counts / offsets and the expert kernel's
+// token-tile schedule and resets its scheduler words. chunk_hist is only read.
+constexpr int kScanSlotsTiles = 18;  // 256 / chunk + 2 for chunk >= 16 entries
+__global__ void __launch_bounds__(256)
+    k_scan_slots(const int32_t* __restrict__ chunk_hist, int nchunks, const int32_t* __restrict__ ids,
+                 const int32_t* __restrict__ rank_local, int S, int E, int topk, int chunk, int max_n,
+                 int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix,
+                 int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched, int32_t* __restrict__ slot_of,
+                 int32_t* __restrict__ tok_of) {
+  __shared__ int32_t s_pre[256], s_tot[256], s_off[256], s_ws[2][8];
+  __shared__ int32_t s_base[kScanSlotsTiles][256];
+  pdl_trigger();
+  pdl_wait();
+  const int tid = threadIdx.x;
+  if (tid == 0) LP_TRACE_MIN(24);
+  const int i0 = blockIdx.x * 256;
+  const int t_lo = i0 / chunk;
+  const int t_hi = min(nchunks - 1, (min(i0 + 255, S - 1)) / chunk);
+  // (1) per expert: sum over tiles < t_lo and over all tiles; 256/e_pad thread groups split the tiles
+  const int e_pad = (E + 31) & ~31;
+  const int G = 256 / e_pad, g = tid / e_pad, e = tid % e_pad;
+  int pre = 0, tot = 0;
+  if (g < G && e < E) {
+    const int per = (nchunks + G - 1) / G;
+    const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(chunk_hist + static_cast<size_t>(c + u) * E + e);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { tot += v[u]; pre += (c + u < t_lo) ? v[u] : 0; }
+    }
+    for (; c < c1; ++c) {
+      const int v = __ldcg(chunk_hist + static_cast<size_t>(c) * E + e);
+      tot += v;
+      pre += (c < t_lo) ? v : 0;
+    }
+  }
+  if (g == 0) { s_pre[e] = 0; s_tot[e] = 0; }
+  __syncthreads();
+  if (g < G && e < E) { atomicAdd(&s_pre[e], pre); atomicAdd(&s_tot[e], tot); }
+  __syncthreads();
+  // (2) bases of this CTA's tiles; offsets and the tile schedule over experts (block scan)
+  const int ntl = t_hi - t_lo + 1;
+  if (tid < e_pad) {
+    int run = s_pre[tid];
+    for (int k = 0; k < ntl; ++k) {
+      s_base[k][tid] = run;
+      if (tid < E && k + 1 < ntl) run += __ldcg(chunk_hist + static_cast<size_t>(t_lo + k) * E + tid);
+    }
+  }
+  const int cnt = (tid < E) ? s_tot[tid] : 0;
+  const int ntiles = (cnt > 0) ? (cnt + max_n - 1) / max_n : 0;
+  int a = cnt, b = ntiles;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ua = __shfl_up_sync(0xffffffffu, a, o);
+    const int ub = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) { a += ua; b += ub; }
+  }
+  if (lane == 31) { s_ws[0][wid] = a; s_ws[1][wid] = b; }
+  __syncthreads();
+  int wa = 0, wb = 0;
+  for (int w = 0; w < wid; ++w) { wa += s_ws[0][w]; wb += s_ws[1][w]; }
+  const int inc_a = a + wa, inc_b = b + wb;
+  s_off[tid] = inc_a - cnt;
+  if (blockIdx.x == 0) {
+    if (tid < E) {
+      counts[tid] = cnt;
+      offsets[tid] = inc_a - cnt;
+      tile_prefix[tid] = inc_b - ntiles;
+      const int rows = ntiles ? (cnt + ntiles - 1) / ntiles : 0;
+      tile_rows[tid] = min(max_n, (rows + 15) & ~15);
+      if (tid == E - 1) { offsets[E] = inc_a; tile_prefix[E] = inc_b; }
+    }
+    for (int k = tid; k <= E; k += 256) sched[k] = 0u;
+  }
+  __syncthreads();
+  // (3) this CTA's entries
+  const int i = i0 + tid;
+  if (i < S) {
+    const int ex = __ldcg(ids + i);
+    const int slot = s_off[ex] + s_base[i / chunk - t_lo][ex] + __ldcg(rank_local + i);
+    slot_of[i] = slot;
+    tok_of[slot] = i / topk;
+  }
+  if (tid == 0) LP_TRACE_MAX(25);
+}
+
 // x_perm[slot] = x[tok_of[slot]] (standalone lp_moe_permute only; the fused
 // forward never materialises x_perm — the expert kernel gathers rows by TMA).
 __global__ void __launch_bounds__(256)

@@ -162,6 +162,25 @@ def test_staged_api_matches_fused(cuda):
     assert mo.rel_l2(y_perm.float().cpu().numpy(), ref["y_perm"]) <= REL_L2_TOL
 
 
+@pytest.mark.parametrize("T", [1, 37, 576, 2500, 8224])
+def test_permute_slot_maps_without_rows(cuda, T):
+    """Index-only permutation (one fused scan + slot-map launch) = the oracle's stable counting sort."""
+    s = QWEN3_30B_A3B
+    _, _, _, layer = make(s, 21, cuda)
+    g = torch.Generator().manual_seed(T)
+    ids = torch.stack([torch.randperm(s.num_experts, generator=g)[: s.top_k] for _ in range(T)]).to(torch.int32)
+    if T >= 3:  # skew: a third of the tokens on 16 hot experts
+        ids[: T // 3] = torch.stack([torch.randperm(16, generator=g)[: s.top_k] for _ in range(T // 3)])
+    counts, offsets, slot_of, tok_of, x_perm = layer.permute(ids.to(cuda), None)
+    torch.cuda.synchronize()
+    assert x_perm is None
+    rc, ro, rs, rt = mo.permute(ids.numpy(), s.num_experts)
+    np.testing.assert_array_equal(counts.cpu().numpy(), rc)
+    np.testing.assert_array_equal(offsets.cpu().numpy(), ro)
+    np.testing.assert_array_equal(slot_of.cpu().numpy(), rs)
+    np.testing.assert_array_equal(tok_of.cpu().numpy(), rt)
+
+
 def test_empty_batch(cuda):
     s = TINY
     _, _, _, layer = make(s, 11, cuda)
@@ -265,7 +284,8 @@ def test_host_pipeline_matches_device_forward(cuda):
 
 
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
-                                  "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0"])
+                                  "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0",
+                                  "LPMOE_SCAN_SLOTS=0"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
