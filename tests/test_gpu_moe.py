@@ -13,7 +13,7 @@ import pytest
 import torch
 
 from oracle import moe_oracle as mo
-from paper_2510_08055_b200 import QWEN3_30B_A3B, TINY, MoEShape
+from paper_2510_08055_b200 import QWEN3_30B_A3B, TINY, MoEShape, _native
 from paper_2510_08055_b200.moe import GpuMoE
 from paper_2510_08055_b200.synthetic import expert_weights, router_tokens, router_weight
 
@@ -179,6 +179,21 @@ def test_permute_slot_maps_without_rows(cuda, T):
     np.testing.assert_array_equal(offsets.cpu().numpy(), ro)
     np.testing.assert_array_equal(slot_of.cpu().numpy(), rs)
     np.testing.assert_array_equal(tok_of.cpu().numpy(), rt)
+
+
+@pytest.mark.parametrize("T,launches", [(1, 4), (576, 4), (4100, 5)])
+def test_forward_launch_count(cuda, T, launches):
+    """One layer = router, scan+slots (or scan, scatter), expert kernel, combine: counted by liblpmoe."""
+    s = QWEN3_30B_A3B
+    _, _, _, layer = make(s, 21, cuda)
+    x = router_tokens(T, s.hidden, 7).to(cuda)
+    layer(x)
+    torch.cuda.synchronize()
+    lib = _native.load()
+    n0 = lib.lp_launch_count()
+    layer(x)
+    torch.cuda.synchronize()
+    assert lib.lp_launch_count() - n0 == launches
 
 
 def test_empty_batch(cuda):
