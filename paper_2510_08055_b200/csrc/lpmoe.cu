@@ -443,8 +443,10 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
   const int S = T * topk;
   const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
   const int chunk = chunk_tokens * topk;
-  if (x_perm == nullptr && zero_n == 0 && use_scan_slots() && S > 0 && 256 / chunk + 2 <= lp::kScanSlotsTiles) {
-    LP_CUDA(launch_pdl(lp::k_scan_slots, (S + 255) / 256, 256, 0, st, static_cast<const int32_t*>(chunk_hist), nchunks,
+  if (x_perm == nullptr && zero_n == 0 && use_scan_slots() && S > 0 &&
+      lp::kScanSlotsThreads / chunk + 2 <= lp::kScanSlotsTiles) {
+    LP_CUDA(launch_pdl(lp::k_scan_slots, (S + lp::kScanSlotsThreads - 1) / lp::kScanSlotsThreads,
+                       lp::kScanSlotsThreads, 0, st, static_cast<const int32_t*>(chunk_hist), nchunks,
                        ids, rank_local, S, E, topk, chunk, max_n, counts, offsets, tile_prefix, tile_rows, sched,
                        slot_of, tok_of));
     return LP_OK;

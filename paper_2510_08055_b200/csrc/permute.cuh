@@ -230,60 +230,67 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) LP_TRACE_MAX(25);
 }
 
-// Scan + slot maps in one launch (gather path: no x_perm). Every CTA owns 256
+// Scan + slot maps in one launch (gather path: no x_perm). Every CTA owns 512
 // routing entries and recomputes, from the router's per-tile histograms, what
 // it needs: per-expert totals -> offsets, and the exclusive bases of the <=
 // kScanSlotsTiles tiles its entries fall in (integer sums: identical to k_scan
 // + k_slots). CTA 0 also publishes counts / offsets and the expert kernel's
 // token-tile schedule and resets its scheduler words. chunk_hist is only read.
-constexpr int kScanSlotsTiles = 18;  // 256 / chunk + 2 for chunk >= 16 entries
-__global__ void __launch_bounds__(256)
+// Latency-bound: every global load of a thread is issued in one batch.
+constexpr int kScanSlotsThreads = 512;
+constexpr int kScanSlotsTiles = 18;  // kScanSlotsThreads / chunk + 2 for chunk >= 32 entries
+__global__ void __launch_bounds__(kScanSlotsThreads)
     k_scan_slots(const int32_t* __restrict__ chunk_hist, int nchunks, const int32_t* __restrict__ ids,
                  const int32_t* __restrict__ rank_local, int S, int E, int topk, int chunk, int max_n,
                  int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix,
                  int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched, int32_t* __restrict__ slot_of,
                  int32_t* __restrict__ tok_of) {
-  __shared__ int32_t s_pre[256], s_tot[256], s_off[256], s_ws[2][8];
+  constexpr int NT = kScanSlotsThreads;
+  __shared__ int32_t s_pre[256], s_tot[256], s_off[256], s_ws[2][NT / 32];
   __shared__ int32_t s_base[kScanSlotsTiles][256];
   pdl_trigger();
   pdl_wait();
   const int tid = threadIdx.x;
   if (tid == 0) LP_TRACE_MIN(24);
-  const int i0 = blockIdx.x * 256;
+  const int i0 = blockIdx.x * NT;
+  const int i = i0 + tid;
   const int t_lo = i0 / chunk;
-  const int t_hi = min(nchunks - 1, (min(i0 + 255, S - 1)) / chunk);
-  // (1) per expert: sum over tiles < t_lo and over all tiles; 256/e_pad thread groups split the tiles
+  const int t_hi = min(nchunks - 1, (min(i0 + NT - 1, S - 1)) / chunk);
+  const int ntl = t_hi - t_lo + 1;
+  // this thread's routing entry, loaded up front
+  const int ex = i < S ? __ldcg(ids + i) : 0;
+  const int rl = i < S ? __ldcg(rank_local + i) : 0;
+  // (1) per expert: sum over tiles < t_lo and over all tiles; NT/e_pad thread groups split the tiles
   const int e_pad = (E + 31) & ~31;
-  const int G = 256 / e_pad, g = tid / e_pad, e = tid % e_pad;
+  const int G = NT / e_pad, g = tid / e_pad, e = tid % e_pad;
   int pre = 0, tot = 0;
   if (g < G && e < E) {
     const int per = (nchunks + G - 1) / G;
     const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
-    int c = c0;
-    for (; c + 8 <= c1; c += 8) {
-      int v[8];
+    for (int c = c0; c < c1; c += 16) {
+      int v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(chunk_hist + static_cast<size_t>(c + u) * E + e);
+      for (int u = 0; u < 16; ++u) v[u] = (c + u < c1) ? __ldcg(chunk_hist + static_cast<size_t>(c + u) * E + e) : 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) { tot += v[u]; pre += (c + u < t_lo) ? v[u] : 0; }
-    }
-    for (; c < c1; ++c) {
-      const int v = __ldcg(chunk_hist + static_cast<size_t>(c) * E + e);
-      tot += v;
-      pre += (c < t_lo) ? v : 0;
+      for (int u = 0; u < 16; ++u) { tot += v[u]; pre += (c + u < t_lo) ? v[u] : 0; }
     }
   }
+  // rows t_lo .. t_hi-1 of the histogram, for the bases of this CTA's tiles
+  int hv[kScanSlotsTiles - 1];
+#pragma unroll
+  for (int k = 0; k < kScanSlotsTiles - 1; ++k)
+    hv[k] = (tid < E && k + 1 < ntl) ? __ldcg(chunk_hist + static_cast<size_t>(t_lo + k) * E + tid) : 0;
   if (g == 0) { s_pre[e] = 0; s_tot[e] = 0; }
   __syncthreads();
   if (g < G && e < E) { atomicAdd(&s_pre[e], pre); atomicAdd(&s_tot[e], tot); }
   __syncthreads();
   // (2) bases of this CTA's tiles; offsets and the tile schedule over experts (block scan)
-  const int ntl = t_hi - t_lo + 1;
   if (tid < e_pad) {
     int run = s_pre[tid];
-    for (int k = 0; k < ntl; ++k) {
-      s_base[k][tid] = run;
-      if (tid < E && k + 1 < ntl) run += __ldcg(chunk_hist + static_cast<size_t>(t_lo + k) * E + tid);
+#pragma unroll
+    for (int k = 0; k < kScanSlotsTiles; ++k) {
+      if (k < ntl) s_base[k][tid] = run;
+      if (k < kScanSlotsTiles - 1) run += hv[k];
     }
   }
   const int cnt = (tid < E) ? s_tot[tid] : 0;
@@ -298,12 +305,12 @@ __global__ void __launch_bounds__(256)
   }
   if (lane == 31) { s_ws[0][wid] = a; s_ws[1][wid] = b; }
   __syncthreads();
-  int wa = 0, wb = 0;
-  for (int w = 0; w < wid; ++w) { wa += s_ws[0][w]; wb += s_ws[1][w]; }
-  const int inc_a = a + wa, inc_b = b + wb;
-  s_off[tid] = inc_a - cnt;
-  if (blockIdx.x == 0) {
-    if (tid < E) {
+  if (tid < 256) {
+    int wa = 0, wb = 0;
+    for (int w = 0; w < wid; ++w) { wa += s_ws[0][w]; wb += s_ws[1][w]; }
+    const int inc_a = a + wa, inc_b = b + wb;
+    s_off[tid] = inc_a - cnt;
+    if (blockIdx.x == 0 && tid < E) {
       counts[tid] = cnt;
       offsets[tid] = inc_a - cnt;
       tile_prefix[tid] = inc_b - ntiles;
@@ -311,14 +318,13 @@ __global__ void __launch_bounds__(256)
       tile_rows[tid] = min(max_n, (rows + 15) & ~15);
       if (tid == E - 1) { offsets[E] = inc_a; tile_prefix[E] = inc_b; }
     }
-    for (int k = tid; k <= E; k += 256) sched[k] = 0u;
   }
+  if (blockIdx.x == 0)
+    for (int k = tid; k <= E; k += NT) sched[k] = 0u;
   __syncthreads();
   // (3) this CTA's entries
-  const int i = i0 + tid;
   if (i < S) {
-    const int ex = __ldcg(ids + i);
-    const int slot = s_off[ex] + s_base[i / chunk - t_lo][ex] + __ldcg(rank_local + i);
+    const int slot = s_off[ex] + s_base[i / chunk - t_lo][ex] + rl;
     slot_of[i] = slot;
     tok_of[slot] = i / topk;
   }
