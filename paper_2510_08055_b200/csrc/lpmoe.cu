@@ -393,7 +393,7 @@ bool fused_route_ok(const Layout& L, int T, int E) {
 
 int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, int renorm, int32_t* ids, float* w,
                  void* ws, const Layout& L, cudaStream_t st, const FusedPermute* fp = nullptr,
-                 const void* warm = nullptr, size_t warm_bytes = 0) {
+                 const void* warm = nullptr, size_t warm_bytes = 0, bool hist = true) {
   int rc;
   if ((rc = get_encode())) return rc;
   const int TN = L.chunk_tokens;
@@ -405,6 +405,10 @@ int launch_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   lp::RouterParams rp{T, H, E, topk, renorm, mtiles, ids, w, at<int32_t>(ws, L.chunk_hist),
                       at<int32_t>(ws, L.rank_local)};
   rp.ntiles = ntiles;
+  if (!hist && !fp) {  // the permutation ranks entries itself (k_scan_slots)
+    rp.tile_hist = nullptr;
+    rp.rank_local = nullptr;
+  }
   rp.warm = static_cast<const uint8_t*>(warm);
   rp.warm_bytes = warm ? warm_bytes : 0;
   const int e_pad = (E + 31) / 32 * 32;
@@ -432,6 +436,16 @@ bool use_scan_slots() {
   return v;
 }
 
+int launch_scan_slots(const int32_t* ids, int T, int E, int topk, int max_n, int32_t* counts, int32_t* offsets,
+                      int32_t* slot_of, int32_t* tok_of, int32_t* tile_prefix, int32_t* tile_rows, uint32_t* sched,
+                      cudaStream_t st) {
+  const int S = T * topk;
+  LP_CUDA(launch_pdl(lp::k_scan_slots, (S + lp::kScanSlotsThreads - 1) / lp::kScanSlotsThreads,
+                     lp::kScanSlotsThreads, 0, st, ids, S, E, topk, max_n, counts, offsets, tile_prefix, tile_rows,
+                     sched, slot_of, tok_of));
+  return LP_OK;
+}
+
 // chunk_hist/rank_local come from the router (forward) or k_chunk_hist (standalone).
 // Scan (one CTA): per-tile bases, counts, offsets, expert tile schedule. Scatter
 // (one warp per routing entry): slot_of / tok_of and, if x_perm, the row copy.
@@ -442,15 +456,6 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
                         int zero_n = 0) {
   const int S = T * topk;
   const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
-  const int chunk = chunk_tokens * topk;
-  if (x_perm == nullptr && zero_n == 0 && use_scan_slots() && S > 0 &&
-      lp::kScanSlotsThreads / chunk + 2 <= lp::kScanSlotsTiles) {
-    LP_CUDA(launch_pdl(lp::k_scan_slots, (S + lp::kScanSlotsThreads - 1) / lp::kScanSlotsThreads,
-                       lp::kScanSlotsThreads, 0, st, static_cast<const int32_t*>(chunk_hist), nchunks,
-                       ids, rank_local, S, E, topk, chunk, max_n, counts, offsets, tile_prefix, tile_rows, sched,
-                       slot_of, tok_of));
-    return LP_OK;
-  }
   const int n_hist = nchunks * E;
   const int smem = n_hist <= lp::kScanSmemInts ? n_hist * 4 : 0;
   if (smem > 48 * 1024) {
@@ -721,6 +726,13 @@ int lp_moe_permute(const int32_t* ids, const void* x, int T, int H, int E, int t
   const Layout L = make_layout(T, H, 128, E, topk);
   if (ws_bytes < L.x_perm) return fail(LP_EINVAL, "lp_moe_permute: workspace %zu < %zu bytes", ws_bytes, L.x_perm);
   const int max_n = pick_max_n(T * topk, E);
+  if (!x_perm && use_scan_slots() && T * topk <= 32768) {  // every CTA reads all ids: small batches only
+    if ((rc = launch_scan_slots(ids, T, E, topk, max_n, counts, offsets, slot_of, tok_of,
+                                at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                at<uint32_t>(ws, L.sched), st)))
+      return rc;
+    return ok();
+  }
   int32_t* chunk_hist = at<int32_t>(ws, L.chunk_hist);
   int32_t* rank_local = at<int32_t>(ws, L.rank_local);
   const int chunk = L.chunk_tokens * topk;
@@ -820,9 +832,16 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
     if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, &fp, w13, warm))) return rc;
     prof_mark(1, st);
   } else {
-    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, nullptr, w13, warm))) return rc;
+    const bool ids_scan = gather && !fused && use_scan_slots();
+    if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, nullptr, w13, warm, !ids_scan)))
+      return rc;
     prof_mark(1, st);
-    if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
+    if (ids_scan) {
+      if ((rc = launch_scan_slots(ids, T, E, topk, max_n, counts, offsets, slot_of, tok_of,
+                                  at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),
+                                  at<uint32_t>(ws, L.sched), st)))
+        return rc;
+    } else if ((rc = launch_scan_scatter(ids, x, T, H, E, topk, L.chunk_tokens, counts, offsets, slot_of, tok_of,
                                   gather ? nullptr : at<void>(ws, L.x_perm),
                                   at<int32_t>(ws, L.chunk_hist), at<int32_t>(ws, L.rank_local), max_n,
                                   at<int32_t>(ws, L.tile_prefix), at<int32_t>(ws, L.tile_rows),

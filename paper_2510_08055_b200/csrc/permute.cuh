@@ -230,73 +230,71 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) LP_TRACE_MAX(25);
 }
 
-// Scan + slot maps in one launch (gather path: no x_perm). Every CTA owns 512
-// routing entries and recomputes, from the router's per-tile histograms, what
-// it needs: per-expert totals -> offsets, and the exclusive bases of the <=
-// kScanSlotsTiles tiles its entries fall in (integer sums: identical to k_scan
-// + k_slots). CTA 0 also publishes counts / offsets and the expert kernel's
-// token-tile schedule and resets its scheduler words. chunk_hist is only read.
-// Latency-bound: every global load of a thread is issued in one batch.
+// Scan + slot maps in one launch, straight from the routing ids (gather path:
+// no x_perm; the router then skips its per-tile histogram). Every CTA owns 512
+// routing entries. It histograms ALL entries (totals -> offsets) and those
+// before its own (the base of each expert's run), and ranks its own entries
+// stably (match_any within a warp, exclusive scan over the 16 warps), so
+//   slot(i) = offsets[e] + #{j < i : ids[j] = e}
+// — the stable counting sort, identical to k_scan + k_slots. CTA 0 also
+// publishes counts / offsets and the expert kernel's token-tile schedule and
+// resets its scheduler words. Latency-bound: loads are issued in batches.
 constexpr int kScanSlotsThreads = 512;
-constexpr int kScanSlotsTiles = 18;  // kScanSlotsThreads / chunk + 2 for chunk >= 32 entries
 __global__ void __launch_bounds__(kScanSlotsThreads)
-    k_scan_slots(const int32_t* __restrict__ chunk_hist, int nchunks, const int32_t* __restrict__ ids,
-                 const int32_t* __restrict__ rank_local, int S, int E, int topk, int chunk, int max_n,
-                 int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix,
-                 int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched, int32_t* __restrict__ slot_of,
-                 int32_t* __restrict__ tok_of) {
-  constexpr int NT = kScanSlotsThreads;
-  __shared__ int32_t s_pre[256], s_tot[256], s_off[256], s_ws[2][NT / 32];
-  __shared__ int32_t s_base[kScanSlotsTiles][256];
+    k_scan_slots(const int32_t* __restrict__ ids, int S, int E, int topk, int max_n, int32_t* __restrict__ counts,
+                 int32_t* __restrict__ offsets, int32_t* __restrict__ tile_prefix, int32_t* __restrict__ tile_rows,
+                 uint32_t* __restrict__ sched, int32_t* __restrict__ slot_of, int32_t* __restrict__ tok_of) {
+  constexpr int NT = kScanSlotsThreads, NW = NT / 32;
+  __shared__ int32_t s_pre[256], s_tot[256], s_off[256], s_ws[2][NW];
+  __shared__ int32_t s_wh[NW][256];
   pdl_trigger();
   pdl_wait();
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) LP_TRACE_MIN(24);
   const int i0 = blockIdx.x * NT;
   const int i = i0 + tid;
-  const int t_lo = i0 / chunk;
-  const int t_hi = min(nchunks - 1, (min(i0 + NT - 1, S - 1)) / chunk);
-  const int ntl = t_hi - t_lo + 1;
-  // this thread's routing entry, loaded up front
-  const int ex = i < S ? __ldcg(ids + i) : 0;
-  const int rl = i < S ? __ldcg(rank_local + i) : 0;
-  // (1) per expert: sum over tiles < t_lo and over all tiles; NT/e_pad thread groups split the tiles
-  const int e_pad = (E + 31) & ~31;
-  const int G = NT / e_pad, g = tid / e_pad, e = tid % e_pad;
-  int pre = 0, tot = 0;
-  if (g < G && e < E) {
-    const int per = (nchunks + G - 1) / G;
-    const int c0 = min(g * per, nchunks), c1 = min(c0 + per, nchunks);
-    for (int c = c0; c < c1; c += 16) {
-      int v[16];
+  const int ex = i < S ? __ldcg(ids + i) : -1;
+  for (int k = tid; k < 256; k += NT) { s_pre[k] = 0; s_tot[k] = 0; }
+  for (int k = tid; k < NW * 256; k += NT) (&s_wh[0][0])[k] = 0;
+  __syncthreads();
+  // (1) histograms of all entries and of the entries before this CTA's (warp-aggregated smem atomics)
+  for (int j0 = 0; j0 < S; j0 += 8 * NT) {
+    int v[8];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = (c + u < c1) ? __ldcg(chunk_hist + static_cast<size_t>(c + u) * E + e) : 0;
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * NT + tid;
+      v[u] = j < S ? __ldcg(ids + j) : -1;
+    }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) { tot += v[u]; pre += (c + u < t_lo) ? v[u] : 0; }
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * NT + tid;
+      const unsigned peers = __match_any_sync(0xffffffffu, v[u]);
+      if (v[u] >= 0 && (__ffs(peers) - 1) == lane) {
+        const int n = __popc(peers);
+        atomicAdd(&s_tot[v[u]], n);
+        if (j < i0) atomicAdd(&s_pre[v[u]], n);  // whole warp is before i0 or not (i0 % 32 == 0)
+      }
     }
   }
-  // rows t_lo .. t_hi-1 of the histogram, for the bases of this CTA's tiles
-  int hv[kScanSlotsTiles - 1];
-#pragma unroll
-  for (int k = 0; k < kScanSlotsTiles - 1; ++k)
-    hv[k] = (tid < E && k + 1 < ntl) ? __ldcg(chunk_hist + static_cast<size_t>(t_lo + k) * E + tid) : 0;
-  if (g == 0) { s_pre[e] = 0; s_tot[e] = 0; }
+  // (2) stable rank of this CTA's entries: within the warp, then across warps
+  const unsigned peers = __match_any_sync(0xffffffffu, ex);
+  const int rank_w = __popc(peers & ((1u << lane) - 1u));
+  if (ex >= 0 && (__ffs(peers) - 1) == lane) s_wh[wid][ex] = __popc(peers);
   __syncthreads();
-  if (g < G && e < E) { atomicAdd(&s_pre[e], pre); atomicAdd(&s_tot[e], tot); }
-  __syncthreads();
-  // (2) bases of this CTA's tiles; offsets and the tile schedule over experts (block scan)
+  const int e_pad = (E + 31) & ~31;
   if (tid < e_pad) {
     int run = s_pre[tid];
 #pragma unroll
-    for (int k = 0; k < kScanSlotsTiles; ++k) {
-      if (k < ntl) s_base[k][tid] = run;
-      if (k < kScanSlotsTiles - 1) run += hv[k];
+    for (int w = 0; w < NW; ++w) {
+      const int c = s_wh[w][tid];
+      s_wh[w][tid] = run;
+      run += c;
     }
   }
+  // (3) offsets and the tile schedule over experts (block scan over <= 256 experts)
   const int cnt = (tid < E) ? s_tot[tid] : 0;
   const int ntiles = (cnt > 0) ? (cnt + max_n - 1) / max_n : 0;
   int a = cnt, b = ntiles;
-  const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int ua = __shfl_up_sync(0xffffffffu, a, o);
@@ -322,9 +320,9 @@ __global__ void __launch_bounds__(kScanSlotsThreads)
   if (blockIdx.x == 0)
     for (int k = tid; k <= E; k += NT) sched[k] = 0u;
   __syncthreads();
-  // (3) this CTA's entries
-  if (i < S) {
-    const int slot = s_off[ex] + s_base[i / chunk - t_lo][ex] + rl;
+  // (4) this CTA's entries
+  if (ex >= 0) {
+    const int slot = s_off[ex] + s_wh[wid][ex] + rank_w;
     slot_of[i] = slot;
     tok_of[slot] = i / topk;
   }

@@ -363,7 +363,9 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
     named_bar_sync(1, kRouterGate);
     if (tk == 0) LP_TRACE_AT(tr, 5);
   }
-  if (warp >= 2 && warp < 6) {
+  // (tile_hist == nullptr: the permutation ranks the entries itself, k_scan_slots)
+  const bool hist = FUSED || p.tile_hist != nullptr;
+  if (hist && warp >= 2 && warp < 6) {
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
     const int tc0 = t0 + cr * TPC;
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(router_threads(TN), 1)
     // (CS > 1: cross-CTA bases are applied after the cluster barrier below)
     for (int st = 0; st < 4; ++st) { s_rank[et * 4 + st] = my_rank[st]; s_ent[et * 4 + st] = my_e[st]; }
   }
-  if constexpr (CS > 1) {
+  if (CS > 1 && hist) {  // uniform across the cluster (same params)
     // tile histogram across the cluster: CTA r adds the totals of ranks < r to
     // its ranks; the last CTA writes the tile total. Fixed order -> stable slots.
     __syncthreads();
