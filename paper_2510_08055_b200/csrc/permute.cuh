@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256)
 // Scan + slot maps in one launch, straight from the routing ids (gather path:
 // no x_perm; the router then skips its per-tile histogram). Every CTA owns 512
 // routing entries. It histograms ALL entries (totals -> offsets) and those
-// before its own (the base of each expert's run), and ranks its own entries
+// before its own (the base of each expert's run; smem atomics), and ranks its own entries
 // stably (match_any within a warp, exclusive scan over the 16 warps), so
 //   slot(i) = offsets[e] + #{j < i : ids[j] = e}
 // — the stable counting sort, identical to k_scan + k_slots. CTA 0 also
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kScanSlotsThreads)
   for (int k = tid; k < 256; k += NT) { s_pre[k] = 0; s_tot[k] = 0; }
   for (int k = tid; k < NW * 256; k += NT) (&s_wh[0][0])[k] = 0;
   __syncthreads();
-  // (1) histograms of all entries and of the entries before this CTA's (warp-aggregated smem atomics)
+  // (1) histograms of all entries and of the entries before this CTA's (smem atomics)
   for (int j0 = 0; j0 < S; j0 += 8 * NT) {
     int v[8];
 #pragma unroll
@@ -268,11 +268,9 @@ __global__ void __launch_bounds__(kScanSlotsThreads)
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int j = j0 + u * NT + tid;
-      const unsigned peers = __match_any_sync(0xffffffffu, v[u]);
-      if (v[u] >= 0 && (__ffs(peers) - 1) == lane) {
-        const int n = __popc(peers);
-        atomicAdd(&s_tot[v[u]], n);
-        if (j < i0) atomicAdd(&s_pre[v[u]], n);  // whole warp is before i0 or not (i0 % 32 == 0)
+      if (v[u] >= 0) {
+        atomicAdd(&s_tot[v[u]], 1);
+        if (j < i0) atomicAdd(&s_pre[v[u]], 1);
       }
     }
   }
