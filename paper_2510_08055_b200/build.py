@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "_lib", "liblpmoe.so")
 SOURCES = ["lpmoe.cu"]
-HEADERS = ["ptx.cuh", "route.cuh", "permute.cuh", "experts_sm100.cuh", "union_counts.cuh", "norm.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))  # every header lpmoe.cu includes
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

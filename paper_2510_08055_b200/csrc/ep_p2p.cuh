@@ -83,12 +83,12 @@ __global__ void k_ep_plan(int32_t* const* __restrict__ peer_inbox, int P, int El
     for (int s = 0; s < rank; ++s) base += c[s * El + el];
     dest_base[i] = base;
   }
-  if (threadIdx.x <= El) {
+  for (int i = threadIdx.x; i <= El; i += blockDim.x) {  // El + 1 entries: El may reach blockDim.x
     const int32_t* c = s_cnt + rank * P * El;
     int o = 0;
-    for (int e2 = 0; e2 < static_cast<int>(threadIdx.x); ++e2)
+    for (int e2 = 0; e2 < i; ++e2)
       for (int s = 0; s < P; ++s) o += c[s * El + e2];
-    off_local[threadIdx.x] = o;
+    off_local[i] = o;
   }
 }
 

@@ -513,8 +513,14 @@ int launch_experts_pair(const void* src, int src_rows, int S, const void* act, c
   constexpr int smem = lp::PairCfg<BN>::kSmemBytes;
   if ((rc = set_smem(lp::k_experts_pair<GATHER, BN>, smem))) return rc;
   const int sms = sm_count();
-  static int max_clusters = -1;  // pairs that fit at once (one CTA per SM)
-  if (max_clusters < 0) {
+  // pairs that fit at once (one CTA per SM), per device and kernel instance
+  static std::mutex mu;
+  static int cached[64] = {};  // 0 = not computed yet
+  int dev = 0;
+  LP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  int& max_clusters = cached[dev & 63];
+  if (max_clusters <= 0) {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -786,8 +792,10 @@ int lp_moe_experts(const void* x_perm, const int32_t* offsets, int S, const void
 int lp_moe_combine(const void* y_perm, const int32_t* slot_of, const float* w, int T, int H, int topk, void* y,
                    void* stream) {
   if (T < 0 || H <= 0 || H % 8 || topk < 1) return fail(LP_EINVAL, "lp_moe_combine: bad shape T=%d H=%d topk=%d", T, H, topk);
+  if (topk > 32) return fail(LP_EUNSUPPORTED, "lp_moe_combine: topk=%d > 32", topk);
   if (T == 0) return ok();
   if (!y_perm || !slot_of || !w || !y) return fail(LP_EINVAL, "lp_moe_combine: null pointer argument");
+  if (!aligned16(y_perm) || !aligned16(y)) return fail(LP_EINVAL, "lp_moe_combine: y_perm and y must be 16-byte aligned");
   if (H / 8 > 32 * lp::kCombineThreads) return fail(LP_EUNSUPPORTED, "lp_moe_combine: H too large");
   LP_CUDA(launch_pdl(lp::k_combine, T, lp::kCombineThreads, 0, static_cast<cudaStream_t>(stream),
                      static_cast<const __nv_bfloat16*>(y_perm), slot_of, w, T, topk, H, static_cast<__nv_bfloat16*>(y)));
@@ -832,7 +840,7 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
     if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, &fp, w13, warm))) return rc;
     prof_mark(1, st);
   } else {
-    const bool ids_scan = gather && !fused && use_scan_slots();
+    const bool ids_scan = gather && !fused && use_scan_slots() && S <= 32768;  // every CTA reads all ids
     if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, st, nullptr, w13, warm, !ids_scan)))
       return rc;
     prof_mark(1, st);

@@ -7,7 +7,7 @@
 // tokens (`torch.where(expert_mask[e])`, modeling_qwen3_moe.py:243) and the
 // order the oracle's stable argsort produces, so slot_of is bit-exact.
 //
-// Chunks are the router's 32-token tiles: the router kernel (route.cuh) emits
+// Chunks are the router's token tiles (16 or 64 tokens): the router kernel (route.cuh) emits
 // each tile's expert histogram and in-tile stable ranks. One single-block scan
 // kernel turns the per-tile counts into per-tile bases (fixed order), the
 // expert offsets, every entry's slot (slot_of) and its inverse (tok_of), the

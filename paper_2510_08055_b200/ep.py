@@ -356,7 +356,8 @@ class PeerEP:
                                         w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
         rg.barrier(st)
         self.last_ids, self.last_weights = ids, w
-        return y, EPStats(counts, rg.off_local[el], counts.view(P, el).sum(1), [], s)
+        # recv_rows: a stream-ordered copy (the region's off_local is rewritten by the next layer)
+        return y, EPStats(counts, rg.off_local[el].clone(), counts.view(P, el).sum(1), [], s)
 
     __call__ = forward
 

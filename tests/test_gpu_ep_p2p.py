@@ -1,11 +1,16 @@
-"""Peer-memory expert parallelism (ep.PeerEP) on one B200 with 2 processes.
+"""Peer-memory expert parallelism (ep.PeerEP): 2 processes on one B200, and one
+process per physical GPU when the box has several.
 
-Two ranks share cuda:0: CUDA IPC maps each rank's symmetric region into the
+Shared-device tests: two ranks share cuda:0: CUDA IPC maps each rank's symmetric region into the
 other process exactly as it would map a peer GPU's memory over NVLink, and the
 device-side barriers, fused dispatch stores and fused combine loads run for
 real (contexts time-slice, so each barrier costs a scheduling quantum — this
 is a protocol test, not a timing). Every rank's output must equal the
 single-GPU layer (GpuMoE) on the same tokens bit for bit.
+
+Physical-device tests (skipped on a 1-GPU box): rank r runs on cuda:r, so the
+system-scope barriers, the dispatch's remote stores and the combine's remote
+loads cross NVLink/NVSwitch between distinct GPUs.
 """
 
 import os
@@ -27,7 +32,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
+def _worker(rank, world, port, shape_name, tokens, skew, layers, q, physical=False):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -39,8 +44,8 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
         from paper_2510_08055_b200.moe import GpuMoE
         from paper_2510_08055_b200.synthetic import expert_weights, router_tokens, router_weight
 
-        torch.cuda.set_device(0)
-        dev = torch.device("cuda", 0)
+        dev = torch.device("cuda", rank if physical else 0)
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         s = {"tiny": TINY, "qwen": QWEN3_30B_A3B, "e256": MoEShape(512, 256, 256, 8, False)}[shape_name]
         wr = router_weight(s.num_experts, s.hidden, 21).float()
@@ -74,13 +79,13 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q):
         q.put((rank, False, traceback.format_exc()[-2000:]))
 
 
-def _run(shape_name, tokens, skew=False, layers=2, world=2):
+def _run(shape_name, tokens, skew=False, layers=2, world=2, physical=False):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape_name, tokens, skew, layers, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape_name, tokens, skew, layers, q, physical))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -115,3 +120,31 @@ def test_peer_ep2_large_uneven_batches_max_experts(cuda):
     """E = 256 (128 per rank), 3001 vs 7 tokens: the owners' expert kernels run large
     expert-major receive buffers (CTA-pair kernel through the staged API)."""
     _run("e256", [3001, 7], layers=1)
+
+
+def test_peer_ep1_max_local_experts(cuda):
+    """world 1 with E = 256 local experts: the plan kernel must write all El + 1 = 257
+    receive offsets with its 256 threads (the last one is the received-row total)."""
+    _run("e256", [500], layers=1, world=1)
+
+
+def _gpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 physical GPUs")
+def test_peer_ep2_physical_gpus_qwen(cuda):
+    """Two distinct GPUs: barriers, remote stores and remote loads over NVLink."""
+    _run("qwen", [576, 300], physical=True)
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 physical GPUs")
+def test_peer_ep2_physical_gpus_skewed(cuda):
+    _run("tiny", [80, 0], skew=True, physical=True)
+
+
+@pytest.mark.skipif(_gpus() < 4, reason="needs 4+ physical GPUs")
+def test_peer_ep_all_physical_gpus_qwen(cuda):
+    """One rank per GPU on the whole box (4 or 8): every rank sends to every peer."""
+    n = 8 if _gpus() >= 8 else 4
+    _run("qwen", [576 - 37 * r for r in range(n)], physical=True, world=n)
