@@ -1,7 +1,8 @@
-"""Roofline cost of one iteration's kernels and the coverage curves it needs.
+"""Roofline cost arithmetic and the coverage curves the coverage models need.
 
-Host-side restatement of the reference's cost arithmetic so the serving engine
-(serving.py) can run on the GPU box, where /root/reference does not exist:
+Host-side restatement of the reference's cost arithmetic (the a2/a5 rows of
+SURVEY §8) for the package's own coverage models (coverage.py), which must run
+on the GPU box without the reference installed:
 
   moe_cost        costmodel.py:57-85   expert bytes = cov*E*bytes_per_expert*layers
   attention_cost  costmodel.py:88-125
@@ -9,11 +10,9 @@ Host-side restatement of the reference's cost arithmetic so the serving engine
   kernel_runtime  costmodel.py:148-152 max(flops/(peak*mfu), bytes/(bw*mbu))
   coverage        coverage.py:38-89    closed form, tokens/expert, table interpolation
 
-Floating-point operations are issued in the reference's order so engine runs
-reproduce the reference's iteration runtimes bit for bit (tests/test_serving.py
-against tests/golden/plans.json). In measured mode (executor.py) the MoE
-entries are replaced by device time of the real layers; attention / dense
-stay modelled (out of scope).
+Floating-point operations are issued in the reference's order (pinned against
+reference outputs by tests/test_coverage.py and tests/test_types.py). Serving
+runs use the reference's own engine and cost model (refdrive.py), not this file.
 """
 
 from __future__ import annotations

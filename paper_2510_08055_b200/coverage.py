@@ -137,6 +137,7 @@ class MeasuredCoverage:
     hidden: torch.Tensor | None = None  # [N, H] bf16 rows to route (cycled if N < routed_tokens)
     seed: int = 0
     last_device_s: float = field(default=0.0, init=False)
+    last_routed: int = field(default=-1, init=False)   # routed_tokens of the last coverage() call
     last_experts_hit: int = field(default=0, init=False)
 
     def _rows(self, n: int) -> torch.Tensor:
@@ -158,6 +159,7 @@ class MeasuredCoverage:
         e1.record(stream)
         e1.synchronize()
         self.last_device_s = e0.elapsed_time(e1) * 1e-3
+        self.last_routed = routed_tokens
         self.last_experts_hit = stats.experts_hit
         return self.last_experts_hit / self.layer.shape.num_experts
 

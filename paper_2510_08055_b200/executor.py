@@ -1,10 +1,12 @@
-"""Layered executor: drives real MoE layers on the B200 from the serving planner.
+"""Layered executor: runs the reference planner's iterations on real MoE layers on the B200.
 
-SURVEY.md §8(f) row 1. `MeasuredCost` plugs into `serving.run` in place of the
-modelled roofline: for every planned iteration (a `BatchPlan`) it runs the
-iteration's MoE work through a stack of resident `GpuMoE` layers and charges
-the measured device time; attention / dense projections stay modelled
-(out of scope) with the reference formulas on B200 peaks.
+SURVEY.md §8(f) row 1. The reference's own engine plans every iteration
+(`moesim.engine.run` -> `scheduler.plan_for`, scheduler.py:286-291) and, inside
+`refdrive.measured_costs(executor=...)`, hands each `BatchPlan`
+(scheduler.py:82-92) to `LayeredExecutor.run_plan`, which runs the iteration's
+MoE work through a stack of resident `GpuMoE` layers and returns the measured
+device time and the experts each layer's routing really hit; attention / dense
+projections stay the reference's modelled costs (out of scope).
 
 Per iteration and per MoE layer l the routed batch is exactly what the
 reference engine charges at engine.py:137-154: every decoding request's token
@@ -23,13 +25,13 @@ decode rows) and a chunked iteration is one.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import torch
 
-from . import costmodel as cm
 from .moe import GpuMoE, Workspace, add_rmsnorm
-from .serving import BatchPlan, ServingState, attention_kernels
 from .synthetic import router_weight
-from .types import ModelSpec, MoEShape
+from .types import MoEShape
 
 
 class _DecodeGraphs:
@@ -150,12 +152,25 @@ class MoEModel:
         return x
 
 
-class MeasuredCost:
-    """serving.run cost plug-in: measured MoE device time + modelled attention/dense."""
+@dataclass
+class MoEIteration:
+    """What one planned iteration's MoE work measured (refdrive turns it into a KernelCost)."""
 
-    def __init__(self, model_spec: ModelSpec, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False):
-        assert stack.num_layers == model_spec.num_layers
-        self.spec, self.stack = model_spec, stack
+    device_s: float            # device time of the MoE layer calls (CUDA events around the segments)
+    routed: list               # routed tokens through each layer (engine.py:137-154 semantics)
+    experts_hit: list          # experts the routing touched in each layer (nnz of the real counts)
+
+
+def _finished(r) -> bool:
+    return getattr(r.phase, "value", r.phase) == "finished"
+
+
+class LayeredExecutor:
+    """Runs a reference `BatchPlan` on the resident layer stack (duck-typed on moesim's SimState:
+    `state.request(rid)` with `input_len` and `phase`)."""
+
+    def __init__(self, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False):
+        self.stack = stack
         self.keep_final_prompt = keep_final_prompt
         self.final_prompt: dict[int, torch.Tensor] = {}
         self.final_decode: dict[int, torch.Tensor] = {}  # last decode hidden row of finished requests
@@ -166,16 +181,15 @@ class MeasuredCost:
         self.embed_seed = embed_seed
         self.iter_log: list[dict] = []
 
-    def _prompt(self, st: ServingState, rid: int) -> torch.Tensor:
+    def _prompt(self, state, rid: int) -> torch.Tensor:
         h = self.stash.get(rid)
-        if h is None:
-            r = st.by_id[rid]
+        if h is None:  # synthetic prompt embedding (no tokenizer / embedding table: out of scope)
             g = torch.Generator(device=self.dev).manual_seed(self.embed_seed * 1_000_003 + rid)
-            h = torch.randn((r.input_len, self.H), generator=g, device=self.dev).to(torch.bfloat16)
+            h = torch.randn((state.request(rid).input_len, self.H), generator=g, device=self.dev).to(torch.bfloat16)
             self.stash[rid] = h
         return h
 
-    def _decode_rows(self, st: ServingState, plan: BatchPlan) -> list[torch.Tensor]:
+    def _decode_rows(self, plan) -> list[torch.Tensor]:
         rows = []
         for rid in plan.decode_ids:
             row = self.decode_row.get(rid)
@@ -188,62 +202,53 @@ class MeasuredCost:
             rows.append(row)
         return rows
 
-    def iteration(self, st: ServingState, plan: BatchPlan, decode_ctx: int) -> list[cm.Kernel]:
-        L = self.spec.num_layers
-        for rid in [k for k in self.stash if st.by_id[k].phase == "finished"]:
+    def run_plan(self, state, plan) -> MoEIteration:
+        L = self.stack.num_layers
+        for rid in [k for k in self.stash if _finished(state.request(k))]:
             h = self.stash.pop(rid)  # prompt finished without a decode step (output_len == 1)
             if self.keep_final_prompt:
                 self.final_prompt[rid] = h
-        dec_rows = self._decode_rows(st, plan)
+        dec_rows = self._decode_rows(plan)
         D = len(dec_rows)
         cuts = sorted({0, L} | {a.layer_start for a in plan.prefill_assignments}
                       | {a.layer_end for a in plan.prefill_assignments})
         counts = torch.zeros((L, self.stack.shape.num_experts), dtype=torch.int32, device=self.dev)
-        routed = plan.layer_token_counts(L)
+        routed = [D] * L
+        for a in plan.prefill_assignments:
+            for layer in range(a.layer_start, a.layer_end):
+                routed[layer] += a.num_tokens
         stream = torch.cuda.current_stream(self.dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        events = []
         dec = torch.stack(dec_rows) if D else torch.empty((0, self.H), dtype=torch.bfloat16, device=self.dev)
         for l0, l1 in zip(cuts, cuts[1:]):
             act = [a for a in plan.prefill_assignments if a.layer_start <= l0 < a.layer_end]
-            parts = [dec] + [self._prompt(st, a.request_id)[a.token_start:a.token_end] for a in act]
+            parts = [dec] + [self._prompt(state, a.request_id)[a.token_start:a.token_end] for a in act]
             if sum(p.shape[0] for p in parts) == 0:
                 continue
             x = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
+            # only the layer calls are timed (not the embedding, the concatenation or the copy-back)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             x = self.stack.run_segment(x, l0, l1, counts)
+            e1.record(stream)
+            events.append((e0, e1))
             dec = x[:D]
             off = D
             for a in act:
                 n = a.num_tokens
-                self._prompt(st, a.request_id)[a.token_start:a.token_end].copy_(x[off:off + n])
+                self._prompt(state, a.request_id)[a.token_start:a.token_end].copy_(x[off:off + n])
                 off += n
-        e1.record(stream)
         for rid, row in zip(plan.decode_ids, dec):
             self.decode_row[rid] = row
         torch.cuda.synchronize(self.dev)
-        moe_s = e0.elapsed_time(e1) * 1e-3
+        moe_s = sum(a.elapsed_time(b) for a, b in events) * 1e-3
         nnz = (counts > 0).sum(dim=1).cpu().tolist()
-        expert_bytes = float(sum(nnz) * self.spec.bytes_per_expert)
-        act_bytes = float(sum(2 * n * self.spec.hidden_dim * self.spec.dtype_bytes for n in routed))
-        flops = float(sum(n * self.spec.top_k * self.spec.flops_per_token_per_expert for n in routed))
-        ks = [cm.Kernel(cm.MOE, flops, expert_bytes + act_bytes, expert_bytes, measured_s=moe_s)]
-        # modelled non-MoE work (same formulas as the reference engine), on B200 peaks
-        scopes: dict[tuple[int, int], int] = {}
-        for a in plan.prefill_assignments:
-            scopes[(a.layer_start, a.layer_end)] = scopes.get((a.layer_start, a.layer_end), 0) + a.num_tokens
-        covered = 0
-        for (ls, le), pf in sorted(scopes.items()):
-            covered += le - ls
-            ks.append(cm.dense_cost(self.spec, D + pf, le - ls))
-        if L - covered > 0 and D > 0:
-            ks.append(cm.dense_cost(self.spec, D, L - covered))
-        ks.extend(attention_kernels(self.spec, plan, decode_ctx))
         self.iter_log.append({"moe_s": moe_s, "routed": routed, "experts_hit": nnz, "decode": D,
                               "prefill_tokens": plan.prefill_tokens})
-        # drop finished requests' state
-        live = {r.id for r in st.decoding} | set(plan.decode_ids)
+        # drop finished requests' state (the engine retires them after this call)
+        live = set(plan.decode_ids) | {r.id for r in state.decoding}
         for rid in [k for k in self.decode_row if k not in live]:
             row = self.decode_row.pop(rid)
             if self.keep_final_prompt:
                 self.final_decode[rid] = row
-        return ks
+        return MoEIteration(moe_s, routed, nnz)

@@ -1,24 +1,47 @@
-"""Layered executor on the B200: real MoE layers driven by the serving planner.
+"""The unmodified reference simulator drives real MoE layers on the B200.
 
-SURVEY §8(d) C1 criterion: layered and chunked prefill run the same per-token
-math, so every prompt's final hidden states must agree — on this GPU path they
-are bit-identical (per-token routing and per-column tcgen05 accumulation do not
-depend on which other tokens share the batch).
+* `moesim.engine.run` plans every iteration (scheduler.plan_for); inside
+  `refdrive.measured_costs(executor=LayeredExecutor(...))` each BatchPlan runs on a
+  resident layer stack. SURVEY §8(d) C1 criterion: layered and chunked prefill run
+  the same per-token math, so every prompt's final hidden states must agree — on
+  this GPU path they are bit-identical (per-token routing and per-column tcgen05
+  accumulation do not depend on which other tokens share the batch).
+* `MeasuredCoverage(layer)` as the engine's / chunk bench's CoverageModel
+  (engine.py:147-153, cli.py:222-227): coverage = nnz(counts)/E of the real routing,
+  MoE runtime = measured device time.
 """
 
 import pytest
 import torch
 
-from paper_2510_08055_b200 import costmodel as cm
-from paper_2510_08055_b200 import serving as sv
-from paper_2510_08055_b200.executor import MeasuredCost, MoEModel
-from paper_2510_08055_b200.types import TINY, ModelSpec
+from paper_2510_08055_b200 import QWEN3_30B_A3B, refdrive
+from paper_2510_08055_b200.coverage import MeasuredCoverage
+from paper_2510_08055_b200.executor import LayeredExecutor, MoEModel
+from paper_2510_08055_b200.moe import GpuMoE
+from paper_2510_08055_b200.synthetic import expert_weights, router_weight
+from paper_2510_08055_b200.types import QWEN3_30B_A3B_MODEL, TINY
 
 pytestmark = pytest.mark.gpu
 
-TINY_MODEL = ModelSpec(name="tiny-moe", num_layers=4, num_experts=16, top_k=2, bytes_per_expert=196608,
-                       dense_bytes_per_layer=524288, flops_per_token_per_expert=196608,
-                       attn_flops_per_token_per_ctx=4096, kv_bytes_per_token=4096, hidden_dim=256)
+if not refdrive.reference_available():
+    pytest.skip("the reference (moesim) is not importable: tools/vendor_reference.sh", allow_module_level=True)
+ms = refdrive.import_moesim()
+
+TINY_MODEL = ms.types.ModelSpec(name="tiny-moe", num_layers=4, num_experts=16, top_k=2, bytes_per_expert=196608,
+                                dense_bytes_per_layer=524288, flops_per_token_per_expert=196608,
+                                attn_flops_per_token_per_ctx=4096, kv_bytes_per_token=4096, hidden_dim=256)
+
+
+def _cfg(policy, chunk=512, target=512):
+    return ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=chunk, group_token_target=target)
+
+
+def _reqs(lens, out):
+    return [ms.types.Request(id=i, arrival_s=0.0, input_len=n, output_len=out) for i, n in enumerate(lens)]
+
+
+def _table():
+    return ms.coverage.EmpiricalTable()
 
 
 @pytest.fixture(scope="module")
@@ -27,55 +50,108 @@ def stack(cuda):
 
 
 def _run(stack, policy, reqs, chunk=512, target=512):
-    cost = MeasuredCost(TINY_MODEL, stack, keep_final_prompt=True)
-    recs, done, makespan = sv.run(TINY_MODEL, cm.B200_MODELLED, sv.Planner(policy, chunk, target), reqs, cost)
-    return recs, done, makespan, cost
+    ex = LayeredExecutor(stack, keep_final_prompt=True)
+    with refdrive.measured_costs(executor=ex):
+        res = ms.engine.run(TINY_MODEL, refdrive.b200_hardware(), _cfg(policy, chunk, target), reqs, _table())
+    return res, ex
 
 
 def test_layered_equals_chunked_final_hidden(stack):
-    reqs = [sv.Request(i, 0.0, n, 4) for i, n in enumerate((1024, 700, 300))]
+    reqs = _reqs((1024, 700, 300), 4)
     lay = _run(stack, "layered", reqs)
     chk = _run(stack, "chunked", reqs)
     hyb = _run(stack, "hybrid", reqs, chunk=256)
     for rid in range(3):
-        a = lay[3].final_prompt[rid]
-        assert torch.equal(a, chk[3].final_prompt[rid]), rid
-        assert torch.equal(a, hyb[3].final_prompt[rid]), rid
+        a = lay[1].final_prompt[rid]
+        assert torch.equal(a, chk[1].final_prompt[rid]), rid
+        assert torch.equal(a, hyb[1].final_prompt[rid]), rid
         assert a.abs().max().item() > 0
 
 
-def test_measured_iterations_follow_the_modelled_plan(stack):
-    reqs = [sv.Request(i, 0.0, n, 6) for i, n in enumerate((1024, 64, 64))]
-    recs, done, _, cost = _run(stack, "layered", reqs)
-    ref, rdone, _ = sv.run(TINY_MODEL, cm.B200_MODELLED, sv.Planner("layered", 512, 512), reqs)
-    assert len(recs) == len(ref) and len(done) == 3
-    assert [r.prefill_tokens for r in recs] == [r.prefill_tokens for r in ref]
-    for rec, log in zip(recs, cost.iter_log):
+def test_measured_iterations_follow_the_reference_plan(stack):
+    reqs = _reqs((1024, 64, 64), 6)
+    res, ex = _run(stack, "layered", reqs)
+    ref = ms.engine.run(TINY_MODEL, refdrive.b200_hardware(), _cfg("layered"), reqs, _table())
+    assert len(res.records) == len(ref.records) and len(res.requests) == 3
+    assert [r.prefill_tokens for r in res.records] == [r.prefill_tokens for r in ref.records]
+    assert [r.designated_group for r in res.records] == [r.designated_group for r in ref.records]
+    for rec, log in zip(res.records, ex.iter_log):
         assert log["moe_s"] > 0
-        assert rec.moe_runtime_s == log["moe_s"]
         # each layer's experts hit never exceed E and cover at least top_k when tokens are routed
         for n, h in zip(log["routed"], log["experts_hit"]):
             assert (h == 0) == (n == 0) and h <= 16 and (n == 0 or h >= 2)
+        # the reference engine records the bytes the GPU routing really loaded (engine.py:251)
         assert rec.expert_load_bytes == sum(log["experts_hit"]) * TINY_MODEL.bytes_per_expert
+        assert rec.runtime_s > log["moe_s"]  # measured MoE + modelled attention/dense
 
 
 def test_decode_graphs_match_eager(cuda):
     """Per-layer CUDA graphs for decode-size segments (MoEModel(graph_tokens=...)) give the
     same hidden states, routing and expert bytes as eager calls."""
     # all arrivals at t=0: the plan stream cannot depend on the measured (graph vs eager) timings
-    reqs = [sv.Request(i, 0.0, n, 7) for i, n in enumerate((700, 40, 300, 5))]
+    reqs = _reqs((700, 40, 300, 5), 7)
     eager = MoEModel(TINY, 4, device=cuda, seed=3)
     graphed = MoEModel(TINY, 4, device=cuda, seed=3, graph_tokens=16)
-    res = []
-    for stack in (eager, graphed):
-        cost = MeasuredCost(TINY_MODEL, stack, keep_final_prompt=True)
-        recs, done, _ = sv.run(TINY_MODEL, cm.B200_MODELLED, sv.Planner("layered", 512, 512), reqs, cost)
-        res.append((recs, cost))
+    res = [_run(s, "layered", reqs) for s in (eager, graphed)]
     (ra, ca), (rb, cb) = res
     assert len(graphed.graphs.graphs) > 0
-    assert [r.expert_load_bytes for r in ra] == [r.expert_load_bytes for r in rb]
+    assert [r.expert_load_bytes for r in ra.records] == [r.expert_load_bytes for r in rb.records]
     assert [g["experts_hit"] for g in ca.iter_log] == [g["experts_hit"] for g in cb.iter_log]
     for rid in range(4):
         assert torch.equal(ca.final_prompt[rid], cb.final_prompt[rid]), rid
         last = [c.final_decode.get(rid, c.decode_row.get(rid)) for c in (ca, cb)]  # finished / still live
         assert last[0] is not None and torch.equal(last[0], last[1]), rid
+
+
+@pytest.fixture(scope="module")
+def qwen_layer(cuda):
+    s = QWEN3_30B_A3B
+    w13, w2 = expert_weights(s.num_experts, s.hidden, s.ffn, 5)
+    return GpuMoE(s, router_weight(s.num_experts, s.hidden, 4).to(cuda), w13.to(cuda), w2.to(cuda))
+
+
+def test_reference_engine_with_measured_coverage(qwen_layer):
+    """moesim.engine.run with MeasuredCoverage as its CoverageModel: every coverage query routes
+    real tokens through the Qwen3-30B-A3B layer; the engine's expert bytes are nnz·bytes_per_expert
+    of that routing and its MoE runtime the measured device time."""
+    cov = MeasuredCoverage(qwen_layer, seed=1)
+    model = refdrive.reference_model(QWEN3_30B_A3B_MODEL)
+    seen = []
+    orig = cov.coverage
+
+    def spy(n, rng=None):
+        c = orig(n, rng)
+        seen.append((n, c, cov.last_experts_hit, cov.last_device_s))
+        return c
+
+    cov.coverage = spy
+    reqs = [ms.types.Request(id=0, arrival_s=0.0, input_len=2048, output_len=3),
+            ms.types.Request(id=1, arrival_s=0.0, input_len=300, output_len=4)]
+    with refdrive.measured_costs(coverage=cov):
+        res = ms.engine.run(model, refdrive.b200_hardware(), _cfg("layered"), reqs, cov)
+    assert seen and len(res.requests) == 2
+    for n, c, hit, dev_s in seen:
+        assert c == hit / 128 and dev_s > 0
+        assert (hit == 0) == (n == 0) and hit <= min(128, 8 * n)
+    # per iteration: expert bytes = Σ_scopes nnz · 9,437,184 · layers_in_scope (costmodel.py:77)
+    assert ms.metrics.expert_load_total(res.records) > 0
+    for rec in res.records:
+        assert rec.expert_load_bytes % model.bytes_per_expert == 0
+
+
+def test_reference_chunk_bench_with_measured_coverage(qwen_layer):
+    """moesim.cli.chunk_bench_rows (cli.py:211-243) with MeasuredCoverage: the MoE column is the
+    measured layer time x 48 layers per chunk, the bytes column nnz·bytes_per_expert·48."""
+    model = refdrive.reference_model(QWEN3_30B_A3B_MODEL)
+    cov = MeasuredCoverage(qwen_layer, seed=2)
+    with refdrive.measured_costs(coverage=cov):
+        rows = ms.cli.chunk_bench_rows(model, refdrive.b200_hardware(), cov, 4096, [512, 4096])
+    modelled = ms.cli.chunk_bench_rows(model, refdrive.b200_hardware(), ms.coverage.UniformAnalytic(8, 128), 4096,
+                                       [512, 4096])
+    for r, m in zip(rows, modelled):
+        assert r["num_chunks"] == m["num_chunks"]
+        # every 512+-token batch hits all 128 experts, as the closed form says (P(miss) ~ 1e-8)
+        assert r["moe_expert_bytes"] == r["num_chunks"] * 128 * model.bytes_per_expert * 48
+        assert r["moe_runtime_s"] > 0 and r["moe_runtime_s"] != m["moe_runtime_s"]
+    # one 4096-token chunk streams the weights once per layer instead of 8 times
+    assert rows[1]["moe_expert_bytes"] * 8 == rows[0]["moe_expert_bytes"]

@@ -1,13 +1,19 @@
-"""Measured layered-vs-chunked serving on one B200 (BASELINE configs 3, 4, 5).
+"""Measured layered-vs-chunked serving on one B200 (BASELINE configs 3, 4, 5), planned and
+clocked by the UNMODIFIED reference engine.
 
 All 48 Qwen3-30B-A3B MoE layers are resident (58 GB of bf16 expert weights,
-random init); every planned iteration runs its MoE work on the GPU
-(executor.MeasuredCost) and charges the measured device time; attention and
-dense projections are modelled on B200 peaks.
+random init). `moesim.engine.run` (engine.py:272-351) plans every iteration with
+the reference's own scheduler; inside `refdrive.measured_costs(executor=...)` the
+iteration's BatchPlan runs through the layer stack on the GPU and the reference
+engine charges the measured MoE device time (attention and dense projections
+stay the reference's modelled costs on B200 peaks). Beside every
+measured run the same request stream is run through the unmodified, fully
+modelled reference on its own h100-like config (configs/h100like.toml, table
+coverage).
 
   python tools/serving_bench.py --config c3        # 8192-token prompt + 32 concurrent decodes
   python tools/serving_bench.py --config c4        # chunk-size / layer-group sweep on an 8192-token prompt
-  python tools/serving_bench.py --config c5 [--requests 100]   # arXiv-length trace (plans.json)
+  python tools/serving_bench.py --config c5 [--requests 100]   # configs/qwen_arxiv_layered.toml workload
 
 Prints one JSON object per run on stdout.
 """
@@ -22,38 +28,50 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from paper_2510_08055_b200 import refdrive  # noqa: E402
 from paper_2510_08055_b200.types import QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL  # noqa: E402
-from paper_2510_08055_b200 import costmodel as cm  # noqa: E402
-from paper_2510_08055_b200 import serving as sv  # noqa: E402
+
+ms = refdrive.import_moesim()
+MODEL = refdrive.reference_model(QWEN3_30B_A3B_MODEL)
+SLO = ms.types.SloSpec(ttft_slo_s=10.0, tbt_slo_s=0.125)  # configs/qwen_arxiv_layered.toml [slo]
 
 
-def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True):
-    from paper_2510_08055_b200.executor import MeasuredCost
+def _h100():
+    return ms.config.load_run_config(refdrive.reference_config("qwen_arxiv_layered.toml")).hardware
 
-    cost = MeasuredCost(QWEN3_30B_A3B_MODEL, stack)
+
+def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, graphs=0):
+    from paper_2510_08055_b200.executor import LayeredExecutor
+
+    cfg = ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=chunk, group_token_target=target)
+    ex = LayeredExecutor(stack)
     t0 = time.time()
-    recs, done, makespan = sv.run(QWEN3_30B_A3B_MODEL, cm.B200_MODELLED, sv.Planner(policy, chunk, target), reqs, cost)
+    with refdrive.measured_costs(executor=ex):
+        res = ms.engine.run(MODEL, refdrive.b200_hardware(), cfg, reqs, ms.coverage.EmpiricalTable())
     wall = time.time() - t0
-    s = sv.summarize(recs, done, makespan)
+    s = ms.metrics.summarize(res, SLO).to_dict()
+    moe_s = sum(it["moe_s"] for it in ex.iter_log)
     out = {"run": name, "policy": policy, "chunk_size": chunk, "group_token_target": target, **s,
-           "expert_load_GB": s["total_expert_load_bytes"] / 1e9, "moe_time_ms": s["moe_time_s"] * 1e3,
-           "wall_s": wall}
+           "expert_load_GB": s["total_expert_load_bytes"] / 1e9, "moe_time_ms": moe_s * 1e3,
+           "moe_us_per_layer_call": 1e6 * moe_s / max(1, sum(sum(1 for n in it["routed"] if n)
+                                                             for it in ex.iter_log)),
+           "decode_graph_tokens": graphs, "wall_s": wall}
     if focus is not None:
-        r = next(r for r in done if r.id == focus)
+        r = next(r for r in res.requests if r.id == focus)
         out["focus_ttft_s"] = r.first_token_s - r.arrival_s
-        pf = [rec for rec in recs if rec.prefill_tokens]
+        pf = [(rec, it) for rec, it in zip(res.records, ex.iter_log) if rec.prefill_tokens]
         out["prefill_iterations"] = len(pf)
-        out["prefill_expert_load_GB"] = sum(rec.expert_load_bytes for rec in pf) / 1e9
-        out["prefill_moe_ms"] = sum(rec.moe_runtime_s for rec in pf) * 1e3
+        out["prefill_expert_load_GB"] = sum(rec.expert_load_bytes for rec, _ in pf) / 1e9
+        out["prefill_moe_ms"] = sum(it["moe_s"] for _, it in pf) * 1e3
         # decode gaps while the long prompt was being prefilled
-        gaps = [rec.runtime_s for rec in pf if rec.decode_batch_size]
+        gaps = [rec.runtime_s for rec, _ in pf if rec.decode_batch_size]
         out["tbt_during_prefill_mean_ms"] = 1e3 * sum(gaps) / len(gaps) if gaps else 0.0
         out["tbt_during_prefill_max_ms"] = 1e3 * max(gaps) if gaps else 0.0
-    # modelled reference numbers for the same plan stream (costmodel on h100-like, table coverage)
-    mrecs, mdone, mspan = sv.run(QWEN3_30B_A3B_MODEL, cm.H100_LIKE, sv.Planner(policy, chunk, target), reqs)
-    ms = sv.summarize(mrecs, mdone, mspan)
-    out["reference_model_h100"] = {k: ms[k] for k in ("ttft_mean_s", "tbt_mean_s", "total_expert_load_bytes",
-                                                      "num_iterations")}
+    # the unmodified reference, fully modelled, on its own h100-like config, same request stream
+    mres = ms.engine.run(MODEL, _h100(), cfg, reqs, ms.coverage.EmpiricalTable())
+    m = ms.metrics.summarize(mres, SLO).to_dict()
+    out["reference_model_h100"] = {k: m[k] for k in ("ttft_mean_s", "tbt_mean_s", "total_expert_load_bytes",
+                                                     "num_iterations")}
     if emit:
         print(json.dumps(out), flush=True)
     return out
@@ -64,47 +82,49 @@ def main():
     ap.add_argument("--config", choices=["c3", "c4", "c5"], default="c3")
     ap.add_argument("--requests", type=int, default=100)
     ap.add_argument("--prompt", type=int, default=8192)
-    ap.add_argument("--graph-tokens", type=int, default=0,
-                    help="capture per-layer CUDA graphs for decode segments up to this many rows (0: eager)")
-    ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (workload.export_trace) instead of "
-                                                 "the committed arXiv request fixture")
+    ap.add_argument("--graph-tokens", type=int, default=16,
+                    help="replay per-layer CUDA graphs for decode segments up to this many rows (0: eager)")
+    ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (moesim workload.export_trace) "
+                                                 "instead of the config's generated workload")
     a = ap.parse_args()
 
     from paper_2510_08055_b200.executor import MoEModel
 
     t0 = time.time()
-    stack = MoEModel(QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL.num_layers, device="cuda", seed=11,
-                     graph_tokens=a.graph_tokens)
+    stack = MoEModel(QWEN3_30B_A3B, MODEL.num_layers, device="cuda", seed=11, graph_tokens=a.graph_tokens)
     if stack.graphs is not None:  # decode-only layer steps replay CUDA graphs (captured up front)
         stack.graphs.capture(range(1, a.graph_tokens + 1))
     print(json.dumps({"setup": "48 resident layers", "seconds": time.time() - t0,
                       "decode_graph_tokens": a.graph_tokens}), flush=True)
+    g = a.graph_tokens
+    R = ms.types.Request
     L = a.prompt
     if a.config == "c3":
-        reqs = [sv.Request(i, 0.0, 128, 256) for i in range(32)] + [sv.Request(32, 0.0005, L, 16)]
+        reqs = [R(id=i, arrival_s=0.0, input_len=128, output_len=256) for i in range(32)]
+        reqs.append(R(id=32, arrival_s=0.0005, input_len=L, output_len=16))
         # untimed warm-up of the first configuration: the first layer call at each new batch
         # size grows the shared workspace and builds tensor maps (one-off host + cudaMalloc cost)
         run_one(stack, "warmup", "layered", 512, 512, reqs, focus=32, emit=False)
         for policy, chunk, target in (("layered", 512, 512), ("chunked", 512, 512), ("chunked", 2048, 512),
                                       ("hybrid", 2048, 512)):
-            run_one(stack, f"c3_{policy}_c{chunk}_g{target}", policy, chunk, target, reqs, focus=32)
+            run_one(stack, f"c3_{policy}_c{chunk}_g{target}", policy, chunk, target, reqs, focus=32, graphs=g)
     elif a.config == "c4":
-        reqs = [sv.Request(0, 0.0, L, 1)]
+        reqs = [R(id=0, arrival_s=0.0, input_len=L, output_len=1)]
         run_one(stack, "warmup", "chunked", 8192, 512, reqs, focus=0, emit=False)
         for chunk in (512, 1024, 2048, 4096, 8192):
-            run_one(stack, f"c4_chunked_c{chunk}", "chunked", chunk, 512, reqs, focus=0)
+            run_one(stack, f"c4_chunked_c{chunk}", "chunked", chunk, 512, reqs, focus=0, graphs=g)
         for groups in (1, 2, 3, 4, 6, 8, 12, 16, 24, 48):
             target = math.ceil(L / groups)
-            run_one(stack, f"c4_layered_G{groups}", "layered", 512, target, reqs, focus=0)
+            run_one(stack, f"c4_layered_G{groups}", "layered", 512, target, reqs, focus=0, graphs=g)
     else:
         if a.trace:
-            reqs = sv.load_trace(a.trace)[: a.requests]
-        else:
-            gold = json.load(open(os.path.join(ROOT, "tests", "golden", "plans.json")))
-            reqs = [sv.Request(i, t, li, lo) for i, t, li, lo in gold["arxiv"]["requests"][: a.requests]]
+            reqs = ms.workload.load_trace(a.trace)[: a.requests]
+        else:  # the reference's own arXiv-shaped workload (lognormal 9194/5754 in, 231/104 out, 1.3 req/s)
+            cfg = ms.config.load_run_config(refdrive.reference_config("qwen_arxiv_layered.toml"))
+            reqs = ms.workload.generate_requests(cfg.workload)[: a.requests]
         run_one(stack, "warmup", "layered", 512, 512, reqs[:10], emit=False)
         for policy in ("layered", "chunked"):
-            run_one(stack, f"c5_{policy}", policy, 512, 512, reqs)
+            run_one(stack, f"c5_{policy}", policy, 512, 512, reqs, graphs=g)
 
 
 if __name__ == "__main__":
