@@ -310,11 +310,17 @@ def run_ours(args, rank: int, world: int):
     clocks.stop()
     # profiling pass over the same K steps: events at the stage boundaries (this
     # serialises the stages, so per-stage times include each kernel's launch)
+    peer = world > 1 and args.ep == "p2p"
     if world == 1:
         for i in range(K):
             lib.lp_profile_events(ptr_arrays[i], 5)
             step(i)
         lib.lp_profile_events(None, 0)
+        torch.cuda.synchronize()
+    elif peer:  # PeerEP records its own stage boundaries
+        barrier()
+        for i in range(K):
+            layers[i % N_LAYER_SETS](xs[i % N_INPUTS], out=ys[i % N_INPUTS], prof=stage_ev[i])
         torch.cuda.synchronize()
     barrier()
     ms = start.elapsed_time(end) / K
@@ -323,14 +329,20 @@ def run_ours(args, rank: int, world: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # per-stage device time (only recorded by the single-GPU fused path)
+    # per-stage device time (single GPU: route | permute | experts | combine; PeerEP: route+permute |
+    # counts+dispatch (with their barriers) | experts (+ barrier) | combine (+ barrier)); max over ranks
     stage_us = None
-    if world == 1:
-        names = ["route", "permute", "experts", "combine"]
+    if world == 1 or peer:
+        names = ["route", "permute", "experts", "combine"] if world == 1 else \
+            ["route_permute", "dispatch", "experts", "combine"]
         sums = [0.0] * 4
         for evs in stage_ev:
             for j in range(4):
                 sums[j] += evs[j].elapsed_time(evs[j + 1])
+        if world > 1:
+            t = torch.tensor(sums, dtype=torch.float64, device="cpu" if _shared_gpu() else dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sums = t.cpu().tolist()
         stage_us = {n: 1e3 * v / K for n, v in zip(names, sums)}
 
     # ---- end-to-end through the public API with host buffers: every step uploads
@@ -369,12 +381,41 @@ def run_ours(args, rank: int, world: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # routing stats for the roofline (same inputs as the timed steps)
-    hits = []
-    if world == 1:
-        for i in range(N_LAYER_SETS):
-            _, st = layers[i](xs[i % N_INPUTS])
+    # ---- per-call latency through the public API: one synchronous forward_host per step
+    # (H2D of x, the layer, D2H of y, nothing overlapped) — what a single caller waits for
+    x_dev1 = torch.empty((T, s.hidden), dtype=torch.bfloat16, device=dev)
+    lat = []
+    barrier()
+    for i in range(max(3, min(K, 20))):
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        layers[i % N_LAYER_SETS].forward_host(xs_host[i % N_INPUTS], y_host, x_dev=x_dev1)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            lat.append(l0.elapsed_time(l1))
+    lat_ms = statistics.median(lat)
+    if world > 1:
+        t = torch.tensor([lat_ms], device="cpu" if _shared_gpu() else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lat_ms = float(t.item())
+
+    # routing stats for the roofline (same inputs as the timed steps): experts this rank's kernel
+    # streams (single GPU: all hit experts; EP: the hit experts it owns) and rows it processes
+    hits, rows = [], []
+    for i in range(N_LAYER_SETS):
+        _, st = layers[i](xs[i % N_INPUTS])
+        if world == 1:
             hits.append(st.experts_hit)
+            rows.append(T * s.top_k)
+        else:
+            c = st.counts.to(torch.int64)
+            c = c.cpu() if _shared_gpu() else c
+            dist.all_reduce(c)
+            el = s.num_experts // world
+            mine = c[rank * el:(rank + 1) * el]
+            hits.append(int((mine > 0).sum()))
+            rows.append(int(mine.sum()))
     torch.cuda.synchronize()
 
     if rank != 0:
@@ -395,7 +436,13 @@ def run_ours(args, rank: int, world: int):
                    "l2": f"inputs larger than L2: {N_LAYER_SETS} layer weight sets "
                          f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
-                "d2h_bytes_per_step": T * s.hidden * 2},
+                "d2h_bytes_per_step": T * s.hidden * 2,
+                "note": "pipelined: step i's H2D/D2H overlap neighbouring steps' layers (moe.HostPipeline)"
+                        if world == 1 else "one forward_host per step (H2D, EP layer, D2H), back to back"},
+        "e2e_latency": {"value": lat_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
+                        "d2h_bytes_per_step": T * s.hidden * 2,
+                        "note": "one synchronous forward_host call (H2D of x, layer, D2H of y, no overlap), "
+                                "median, max over ranks"},
         # our kernels launched inside the timed region, counted by liblpmoe (lp_launch_count):
         # single GPU 4 per step (router, scan+slots, experts, combine) in the gather regime,
         # 5 with x_perm (router, scan, scatter, experts, combine); EP adds its plan/dispatch/
@@ -405,13 +452,16 @@ def run_ours(args, rank: int, world: int):
     }
     if stage_us is not None:
         nnz = statistics.mean(hits)
-        algo_bytes = nnz * s.bytes_per_expert + 2 * T * s.hidden * 2
+        R = statistics.mean(rows)  # token rows through this rank's expert kernel
+        # single GPU (gather regime): the kernel reads each token row from x once and writes y_perm rows
+        # at slot granularity; with EP the rows it reads are the received ones
+        algo_bytes = nnz * s.bytes_per_expert + (2 * T * s.hidden * 2 if world == 1 else 2 * R * s.hidden * 2)
         achieved = algo_bytes / (stage_us["experts"] * 1e-6) / 1e9
         traffic, traffic_src = ncu_traffic(T)
         if traffic_src:
             traffic_src += " (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         layer_bytes = nnz * s.bytes_per_expert + s.num_experts * s.hidden * 2 + 2 * T * s.hidden * 2 + T * s.top_k * 8
-        flops = 2.0 * T * s.top_k * 3 * s.hidden * s.ffn  # expert GEMMs (gate/up + down)
+        flops = 2.0 * R * 3 * s.hidden * s.ffn  # expert GEMMs (gate/up + down) of this rank's rows
         tpeak, tpeak_src = measured_tensor_peak()
         kernel = ("k_experts / k_experts_pair (grouped gate/up+SiLU*mul and down, tcgen05); duration from CUDA "
                   "events around its launch in a second pass over the same K steps")
@@ -429,6 +479,10 @@ def run_ours(args, rank: int, world: int):
                                "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                                "algo_bytes_per_launch": algo_bytes,
                                "layer_frac": (layer_bytes / (ms * 1e-3)) / 1e9 / peak}
+        if world > 1:
+            out["roofline"]["per_rank"] = (f"rank {rank}: its {s.num_experts // world} experts ({nnz:g} hit) and "
+                                           f"{R:g} received rows; stage times max over ranks")
+            out["roofline"].pop("layer_frac", None)
         out["stages_us"] = stage_us
         out["experts_hit_mean"] = nnz
     if not args.no_cpu_baseline and world == 1:  # the CPU baseline is a rank-0, N=1 measurement
@@ -447,10 +501,27 @@ def _local_device() -> int:
     return 0 if _shared_gpu() else int(os.environ.get("LOCAL_RANK", 0))
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # `python bench.py --gpus N` without a launcher: start the N ranks ourselves (torchrun, one
+        # process per GPU, rendezvous on 127.0.0.1) and exit with their status
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

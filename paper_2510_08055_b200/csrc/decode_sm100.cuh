@@ -1,0 +1,664 @@
+// Decode-size MoE layer in ONE launch: router + top-k + permutation + grouped
+// expert FFN (K1 + K2 + K3) for T <= 16 tokens with T*topk <= E <= 128 — the
+// decode-only layers of a layered-prefill iteration.
+//
+// Why: at T = 1 the separate launches spent ~12 us routing before any expert
+// weight streamed (router 7 us, scan+slots 2 us, launch gaps), against ~12 us
+// of weight streaming at the HBM roofline (8 experts x 9.4 MB). Here:
+//
+//  * Routing is computed redundantly by every CTA pair (cluster of 2, always
+//    co-resident, so all 148 SMs stream afterwards): CTA r of the pair
+//    computes the router's fixed partial sums 2r and 2r+1 of K = H (each
+//    k-blocks [p*H/256, (p+1)*H/256)) with exactly the router's tcgen05 MMA
+//    chain (M = 128 expert rows of Wr, N = 16 tokens, SWIZZLE_128B, same K
+//    order, one TMEM accumulator per partial), the partials are folded over
+//    DSMEM in part order (p0 + p1 + p2 + p3, as k_router<4, 4, 16> folds its
+//    four CTAs' partials) and every CTA runs the router's own
+//    topk_lanes<32, 4> on the folded fp32 logits: ids, weights and logits are
+//    bit-identical to k_router at this T, with no inter-cluster dependency.
+//    Wr k-blocks are requested before griddepcontrol.wait (weights do not
+//    depend on the predecessor), the token rows after it.
+//  * Every CTA derives the stable permutation (slot = offsets[e] + #{j < i :
+//    ids[j] = e}, match_any within a warp + per-warp prefix) and the work-item
+//    list in shared memory; CTA 0 publishes ids, w, counts, offsets, slot_of
+//    and tok_of for k_combine and the caller.
+//  * The expert stream is k_experts_tiny's (identical MMAs and epilogue, so a
+//    token's rows are bit-identical to the other expert kernels): UP items of
+//    64 act features (64 gate + 64 up rows, one 128-row tile, K = H), DN items
+//    of 128 W2 rows (K = I), items claimed dynamically (deadlock-free without
+//    co-residency: all UP items precede all DN items). NEW: a DN item's W2
+//    tiles are requested into the ring BEFORE its UP dependency resolves (the
+//    act rows follow once it does), and when the hit experts' W2 is small
+//    (<= kW2WarmBytes) it is bulk-prefetched into L2 while the UP items
+//    stream, so the DN phase no longer starts from HBM.
+//  * Scheduler words are left zero: the last CTA to finish resets them.
+//
+// Warp roles (256 threads): w0 TMA producer + scheduler (lane 1: W2 L2
+// prefetch), w1 MMA issuer, w2 TMEM allocator, w2-w3 token-row gather,
+// w4-w7 TMEM drain / epilogue; all 8 warps fold, gate and permute.
+#pragma once
+#include <cuda_bf16.h>
+#include "experts_sm100.cuh"
+#include "ptx.cuh"
+#include "route.cuh"
+
+namespace lp {
+
+struct DecodeCfg {
+  static constexpr int kThreads = 256;
+  static constexpr int kParts = 4;     // the router's fixed K partial sums
+  static constexpr int kMaxPpc = 2;    // partials per CTA at the smallest cluster (2)
+  static constexpr int kN = 16;        // token rows per item (MMA N) = the router tile
+  static constexpr int kMaxT = 16;
+  static constexpr int kMaxE = 128;    // one router m-tile
+  static constexpr int kBBytes = kN * 128;
+  static constexpr int kStageBytes = kATileBytes + kBBytes;  // 18 KiB (1024-aligned)
+  static constexpr int kStages = 11;
+  static constexpr int kAcc = 2;
+  static constexpr int kTmemCols = 32;
+  static constexpr int kXBytes = 64 * kN * 4;                // up values handed to the gate warps
+  static constexpr int kPartBytes = kMaxPpc * kMaxT * kMaxE * 4;  // this CTA's partial logits (read over DSMEM)
+  static constexpr int kLogitBytes = kMaxT * kMaxE * 4;      // folded logits
+  static constexpr int kTopBytes = 2 * kMaxT * 32 * 4;       // selected ids / probabilities
+  // off[E+1] cnt[E] hit[E] tok[S] ent[S] slot[S] + per-warp counts [4][E] + 16 scalars
+  // ... + routing weights w[S] + the fused combine's finished-token lists [2][kMaxT + 1] (+ padding)
+  static constexpr int kPermBytes = 4 * ((kMaxE + 1) + 5 * kMaxE + 4 * kMaxE + 19 + kMaxE + 40);  // 16-B multiple
+  static constexpr int kBarBytes = 8 * (3 * kStages + 1 + 2 * kAcc + 2 * kRing) + 16 * kRing + 16;
+  // folded logits + top-k scratch alias ring stage 0: used only between the routing MMAs' completion
+  // and the first streaming load
+  static_assert(kLogitBytes + kTopBytes <= kStageBytes, "routing scratch fits one ring stage");
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kXBytes + kPartBytes + kPermBytes + kBarBytes;
+  static constexpr int kExitWord = 1 + kMaxExperts + 8;  // sched word counting finished CTAs
+};
+static_assert(DecodeCfg::kSmemBytes <= 232448, "decode kernel shared memory");
+static_assert(DecodeCfg::kPermBytes % 16 == 0, "barrier / ring alignment");
+
+// hit experts' W2 below this many bytes is warmed in L2 during the UP phase
+constexpr size_t kW2WarmBytes = 40u << 20;
+
+struct DecodeParams {
+  int T, H, I, E, topk, renorm;
+  const __nv_bfloat16* x;  // [T, H]
+  const uint8_t* w2;       // [E, H, I] bf16 (L2 warm-up addresses)
+  int32_t* ids;            // [T, topk]
+  float* w;                // [T, topk]
+  int32_t* counts;         // [E]
+  int32_t* offsets;        // [E+1]
+  int32_t* slot_of;        // [T*topk]
+  int32_t* tok_of;         // [T*topk]
+  __nv_bfloat16* act;      // [S, I]
+  __nv_bfloat16* y_perm;   // [S, H]
+  uint32_t* sched;         // [0] item counter, [1+e] UP items done, [kExitWord] finished CTAs
+  __nv_bfloat16* y;        // [T, H] combined output (nullptr: the caller runs k_combine)
+  uint32_t* cmb;           // [T * H/256] fused-combine counters, zero on entry and left zero
+  int weights_evict_first;
+  int warm_w2;             // 1: L2-prefetch the hit experts' W2 when small
+};
+
+__device__ __forceinline__ void cluster_arrive_rel() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+// only orders "my DSMEM reads are done" (their values were consumed): no release needed
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acq() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// CS: CTAs per cluster (2: pairs, always co-resident, every SM streams; 4: each CTA computes one
+// partial (half the Wr bytes per CTA, shorter routing), but 4-CTA clusters leave some SMs unused
+// on a B200 (GPC boundaries) — the host picks 4 for latency-bound tiny batches)
+template <int CS>
+__global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
+    k_decode(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
+             const __grid_constant__ CUtensorMap tm_w13h, const __grid_constant__ CUtensorMap tm_w2,
+             const __grid_constant__ CUtensorMap tm_act, const DecodeParams p) {
+  using C = DecodeCfg;
+  constexpr int kCl = CS;                 // CTAs per cluster
+  constexpr int kPpc = C::kParts / CS;    // partial sums per CTA
+  static_assert(kPpc <= C::kMaxPpc, "partials per CTA");
+  constexpr int S_ = C::kStages;
+  constexpr int A_ = C::kAcc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* cur = smem + S_ * C::kStageBytes;
+  float* xbuf = reinterpret_cast<float*>(cur);        cur += C::kXBytes;     // [16 cols][64 lanes]
+  float* s_part = reinterpret_cast<float*>(cur);      cur += C::kPartBytes;  // [ppc][16 tokens][128 experts]
+  float* s_logit = reinterpret_cast<float*>(smem);                           // [16][128] (ring stage 0)
+  int32_t* s_ids = reinterpret_cast<int32_t*>(smem + C::kLogitBytes);        // [16][32]
+  float* s_p = reinterpret_cast<float*>(s_ids + C::kMaxT * 32);              // [16][32]
+  int32_t* s_off = reinterpret_cast<int32_t*>(cur);   // [E+1]
+  int32_t* s_cnt = s_off + (C::kMaxE + 1);            // [E]
+  int32_t* s_hit = s_cnt + C::kMaxE;                  // [nnz] hit experts, ascending
+  int32_t* s_tok = s_hit + C::kMaxE;                  // [S] token of each slot
+  int32_t* s_ent = s_tok + C::kMaxE;                  // [S] expert of each routing entry
+  int32_t* s_slot = s_ent + C::kMaxE;                 // [S] slot of each routing entry
+  int32_t* s_wc = s_slot + C::kMaxE;                  // [4][E] per-warp counts, then exclusive bases
+  int32_t* s_scal = s_wc + 4 * C::kMaxE;              // [0] nnz, [4..7] warp sums, [8..11] warp hit counts
+  float* s_w = reinterpret_cast<float*>(s_scal + 19);  // [S] routing weights (every CTA)
+  int32_t* s_fin = reinterpret_cast<int32_t*>(s_w + C::kMaxE);  // [2][kMaxT + 1] combine: finished tokens, count
+  cur += C::kPermBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(cur);
+  uint64_t* empty = full + S_;
+  uint64_t* bfull = empty + S_;
+  uint64_t* tfull = bfull + S_ + 1;
+  uint64_t* tempty = tfull + A_;
+  uint64_t* sfull = tempty + A_;
+  uint64_t* sempty = sfull + kRing;
+  int4* ring = reinterpret_cast<int4*>(sempty + kRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+
+  const int warp = warp_idx();
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const int E = p.E, T = p.T, K = p.topk, S = T * K;
+  const int cr = static_cast<int>(cluster_ctarank());
+  const int kbp = p.H / 256;  // k-blocks per partial sum (4 fixed partials of K = H)
+  const int kbr = kPpc * kbp;  // routing k-blocks of this CTA: partials kPpc*cr .. kPpc*cr+kPpc-1
+  [[maybe_unused]] const bool tr = blockIdx.x == 0;  // trace builds only
+  if (tid == 0) LP_TRACE_MIN(48);
+
+  if (tid == 0) {
+    for (int s = 0; s < S_; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&bfull[s], kGatherThreads);
+    }
+    for (int a = 0; a < A_; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int r = 0; r < kRing; ++r) { mbar_init(&sfull[r], 1); mbar_init(&sempty[r], 4); }  // MMA, epi, 2 gather
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_wr); prefetch_tmap(&tm_x); prefetch_tmap(&tm_w13h); prefetch_tmap(&tm_w2);
+    prefetch_tmap(&tm_act);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // Pipeline positions carried from the routing item into the expert stream.
+  int stage = 0; uint32_t phase = 0;  // ring (producer / MMA / gather each keep their own copy)
+  int acc = 0; uint32_t aph = 0;      // TMEM accumulators (MMA / epilogue)
+
+  // =============================== routing: partial sum `cr` of the logits ===============================
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      const int npre = kbr < S_ ? kbr : S_;
+      for (int i = 0; i < npre; ++i) {  // Wr before griddepcontrol.wait: weights never depend on the predecessor
+        mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+        tma_load_2d(smem + i * C::kStageBytes, &tm_wr, &full[i], (cr * kbr + i) * kTileK, 0, pol);
+      }
+      pdl_wait();
+      LP_TRACE_AT(tr, 54);
+      for (int i = 0; i < npre; ++i)
+        tma_load_2d(smem + i * C::kStageBytes + kATileBytes, &tm_x, &full[i], (cr * kbr + i) * kTileK, 0, pol);
+      stage = npre % S_;
+      phase = npre == S_ ? 1u : 0u;
+      for (int i = npre; i < kbr; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::kStageBytes;
+        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+        tma_load_2d(sa, &tm_wr, &full[stage], (cr * kbr + i) * kTileK, 0, pol);
+        tma_load_2d(sa + kATileBytes, &tm_x, &full[stage], (cr * kbr + i) * kTileK, 0, pol);
+        if (++stage == S_) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, C::kN);
+      for (int i = 0; i < kbr; ++i) {  // partial (i / kbp) accumulates in TMEM columns 16 * (i / kbp)
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&bfull[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+        const uint64_t a0 = sdesc_kmajor_sw128(sa);
+        const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
+        const uint32_t d = tmem_base + (i / kbp) * C::kN;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((i % kbp) | k) != 0);
+        mma_commit(&empty[stage]);
+        if (++stage == S_) { stage = 0; phase ^= 1; }
+      }
+      mma_commit(&tfull[0]);
+    }
+  } else if (warp == 2 || warp == 3) {
+    for (int i = 0; i < kbr; ++i) {  // routing operands come by TMA: keep bfull's phases in step
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_arrive(&bfull[stage]);
+      cp_async_commit();  // one (empty) group per stage, as in the stream below
+      if (++stage == S_) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    const int q = warp & 3;
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    const int e = 32 * q + lane;
+#pragma unroll
+    for (int pl = 0; pl < kPpc; ++pl) {
+      uint32_t v[16];
+      tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + pl * C::kN, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s_part[(pl * C::kMaxT + i) * C::kMaxE + e] = __uint_as_float(v[i]);
+    }
+    tc_fence_before();
+    mbar_arrive(&tempty[0]);
+    if (tid == 128) LP_TRACE_AT(tr, 49);
+  }
+  // ring / accumulator positions after the routing item (every role advanced through kbr stages)
+  stage = kbr % S_;
+  phase = (kbr / S_) & 1;
+  acc = 1;
+  aph = 0;
+  pdl_wait();
+  __syncthreads();
+  cluster_arrive_rel();  // this CTA's partial is readable over DSMEM
+  cluster_wait_acq();
+
+  // fold the 4 partials in global part order p0 + p1 + p2 + p3 (rank r holds parts kPpc*r ..), exactly
+  // as k_router<4, 4, 16> folds its four CTAs' partials
+  for (int idx = tid; idx < T * (C::kMaxE / 4); idx += C::kThreads) {
+    const int t = idx / (C::kMaxE / 4), e4 = (idx % (C::kMaxE / 4)) * 4;
+    float4 v[C::kParts];
+#pragma unroll
+    for (int r = 0; r < kCl; ++r)
+#pragma unroll
+      for (int pl = 0; pl < kPpc; ++pl)
+        v[r * kPpc + pl] =
+            ld_dsmem_f4(mapa_shared(smem_u32(s_part + (pl * C::kMaxT + t) * C::kMaxE + e4), r));
+    float4 a = v[0];
+#pragma unroll
+    for (int i = 1; i < C::kParts; ++i) { a.x += v[i].x; a.y += v[i].y; a.z += v[i].z; a.w += v[i].w; }
+    *reinterpret_cast<float4*>(s_logit + t * C::kMaxE + e4) = a;
+  }
+  __syncthreads();
+  if (tid == 0) LP_TRACE_AT(tr, 50);
+  cluster_arrive_relaxed();  // remote partials consumed (matched by the wait before exit)
+  if (tid == 0) LP_TRACE_AT(tr, 57);
+
+  // softmax + top-k: one warp per token (the router's LPT = 32 at this tile shape)
+  for (int g = warp; g < T; g += C::kThreads / 32) {
+    float psum, inv;
+    topk_lanes<32, 4>(s_logit + g * C::kMaxE, E, K, lane, s_ids + g * 32, s_p + g * 32, psum, inv);
+    __syncwarp();
+    for (int r = lane; r < K; r += 32) {
+      const int id = s_ids[g * 32 + r];
+      const float wt = p.renorm ? s_p[g * 32 + r] / psum : s_p[g * 32 + r] * inv;
+      s_ent[g * K + r] = id;
+      s_w[g * K + r] = wt;
+      if (blockIdx.x == 0) {
+        p.ids[static_cast<size_t>(g) * K + r] = id;
+        p.w[static_cast<size_t>(g) * K + r] = wt;
+      }
+    }
+  }
+  if (tid == 0) LP_TRACE_AT(tr, 55);
+  for (int i = tid; i < 4 * C::kMaxE; i += C::kThreads) s_wc[i] = 0;
+  __syncthreads();
+  if (tid == 0) LP_TRACE_AT(tr, 56);
+
+  // stable counting sort of the S <= 128 routing entries (warps 0-3 own entries 32w..32w+31)
+  int my_e = -1, my_rank = 0;
+  if (warp < 4) {
+    my_e = tid < S ? s_ent[tid] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, my_e);
+    my_rank = __popc(peers & ((1u << lane) - 1u));
+    if (my_e >= 0 && (__ffs(peers) - 1) == lane) s_wc[warp * C::kMaxE + my_e] = __popc(peers);
+  }
+  __syncthreads();
+  if (tid < C::kMaxE) {  // per expert: exclusive bases over the 4 warps, total count
+    int run = 0;
+#pragma unroll
+    for (int w4 = 0; w4 < 4; ++w4) {
+      const int c = s_wc[w4 * C::kMaxE + tid];
+      s_wc[w4 * C::kMaxE + tid] = run;
+      run += c;
+    }
+    s_cnt[tid] = tid < E ? run : 0;
+  }
+  __syncthreads();
+  if (warp < 4) {  // exclusive scan of counts over experts (4 warps x 32) + the hit-expert list
+    const int c = s_cnt[tid];
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, c > 0);
+    if (lane == 31) { s_scal[4 + warp] = inc; s_scal[8 + warp] = __popc(hb); }
+    named_bar_sync(3, 128);
+    int base = 0, hbase = 0;
+    for (int w4 = 0; w4 < warp; ++w4) { base += s_scal[4 + w4]; hbase += s_scal[8 + w4]; }
+    if (tid < E) s_off[tid] = base + inc - c;
+    if (tid == 0) s_off[E] = S;
+    if (c > 0) s_hit[hbase + __popc(hb & ((1u << lane) - 1u))] = tid;
+    if (tid == 127) s_scal[0] = hbase + __popc(hb);
+  }
+  __syncthreads();
+  if (my_e >= 0) {
+    const int slot = s_off[my_e] + s_wc[warp * C::kMaxE + my_e] + my_rank;
+    s_slot[tid] = slot;
+    s_tok[slot] = tid / K;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {  // publish the permutation (k_combine, the caller's stats)
+    for (int i = tid; i < S; i += C::kThreads) {
+      p.slot_of[i] = s_slot[i];
+      p.tok_of[i] = s_tok[i];
+    }
+    for (int i = tid; i < E; i += C::kThreads) p.counts[i] = s_cnt[i];
+    for (int i = tid; i <= E; i += C::kThreads) p.offsets[i] = s_off[i];
+  }
+
+  if (tid == 0) LP_TRACE_AT(tr, 51);
+  const int nnz = s_scal[0];
+  const int mt_up = p.I / 64;
+  const int mt_dn = (p.H + kTileM - 1) / kTileM;
+  const int n_up = mt_up * nnz;
+  const int n_items = (mt_up + mt_dn) * nnz;
+
+  // =============================== expert stream (k_experts_tiny's pipeline) ===============================
+  if (warp == 0) {
+    if (lane == 1 && p.warm_w2) {
+      // warm the hit experts' W2 in L2 while the UP items stream (this CTA's share of the union)
+      const size_t per_e = static_cast<size_t>(p.H) * p.I * 2;
+      const size_t total = per_e * nnz;
+      if (total <= kW2WarmBytes) {
+        const size_t share = ((total + gridDim.x - 1) / gridDim.x + 4095) & ~size_t(4095);
+        size_t lo = share * blockIdx.x;
+        const size_t hi = min(total, lo + share);
+        while (lo < hi) {
+          const size_t k = lo / per_e, o = lo - k * per_e;
+          const size_t n = min(min(hi - lo, per_e - o), size_t(65536));
+          bulk_prefetch_l2(p.w2 + static_cast<size_t>(s_hit[k]) * per_e + o, static_cast<uint32_t>(n));
+          lo += n;
+        }
+      }
+    }
+    if (lane == 0) {
+      const uint64_t pol_w = p.weights_evict_first ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_a = policy_evict_last();
+      int r = 0; uint32_t rph = 0;
+      [[maybe_unused]] int n_item = 0;
+      while (true) {
+        const int it = static_cast<int>(atomicAdd(&p.sched[0], 1u));  // every item claimed dynamically
+        if (n_item == 0) LP_TRACE_MIN(52);
+        LP_ITEM(n_item, 0, static_cast<unsigned long long>(it));
+        LP_ITEM(n_item, 1, LP_NOW());
+        int4 info;
+        if (it >= n_items) {
+          info = make_int4(kItemEnd, 0, 0, 0);
+        } else {
+          const bool up = it < n_up;
+          const int mtc = up ? mt_up : mt_dn;
+          const int local = up ? it : it - n_up;
+          const int e = s_hit[local / mtc];
+          const int mt = local % mtc;
+          info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * (up ? 64 : kTileM), s_off[e], s_cnt[e]);
+        }
+        mbar_wait(&sempty[r], rph ^ 1);
+        ring[r] = info;
+        mbar_arrive(&sfull[r]);
+        if (++r == kRing) { r = 0; rph ^= 1; }
+        const int kind = info.x & 0xff;
+        if (kind == kItemEnd) break;
+        const int e = info.x >> 8, m0 = info.y, row0 = info.z;
+        if (kind == kItemUp) {
+          LP_ITEM(n_item, 2, LP_NOW());
+          for (int kb = 0; kb < p.H / kTileK; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::kStageBytes;
+            mbar_arrive_expect_tx(&full[stage], kATileBytes);
+            // rows 0-63: gate features m0..m0+63, rows 64-127: the matching up rows
+            tma_load_2d(sa, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + m0, pol_w);
+            tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + p.I + m0, pol_w);
+            if (++stage == S_) { stage = 0; phase ^= 1; }
+          }
+        } else {
+          // W2 tiles first (they do not depend on the UP items), the act rows once expert e's act is final
+          const int kblocks = p.I / kTileK;
+          const int npre = kblocks < S_ ? kblocks : S_;
+          const int st0 = stage;
+          for (int kb = 0; kb < npre; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+            tma_load_2d(smem + stage * C::kStageBytes, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
+            if (++stage == S_) { stage = 0; phase ^= 1; }
+          }
+          while (ld_acquire_u32(&p.sched[1 + e]) < static_cast<uint32_t>(mt_up)) __nanosleep(32);
+          fence_proxy_async_global();
+          LP_ITEM(n_item, 2, LP_NOW());
+          for (int kb = 0, s = st0; kb < npre; ++kb) {
+            tma_load_2d(smem + s * C::kStageBytes + kATileBytes, &tm_act, &full[s], kb * kTileK, row0, pol_a);
+            if (++s == S_) s = 0;
+          }
+          for (int kb = npre; kb < kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::kStageBytes;
+            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+            tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
+            tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, row0, pol_a);
+            if (++stage == S_) { stage = 0; phase ^= 1; }
+          }
+        }
+        LP_ITEM(n_item, 3, LP_NOW());
+        ++n_item;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int r = 0; uint32_t rph = 0;
+      while (true) {
+        mbar_wait(&sfull[r], rph);
+        const int4 info = ring[r];
+        mbar_arrive(&sempty[r]);
+        if (++r == kRing) { r = 0; rph ^= 1; }
+        const int kind = info.x & 0xff;
+        if (kind == kItemEnd) break;
+        const bool up = kind == kItemUp;
+        const uint32_t idesc = idesc_bf16_f32(kTileM, (info.w + 15) & ~15);
+        const int kblocks = up ? p.H / kTileK : p.I / kTileK;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * C::kN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&bfull[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+          const uint64_t a0 = sdesc_kmajor_sw128(sa);
+          const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kTileK / 16; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == A_) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2 || warp == 3) {
+    // token-row gather for UP items (DN rows come by TMA): 16-byte cp.async into the SWIZZLE_128B layout
+    constexpr int RPT = C::kN / 8;
+    const int gt = tid - 64;
+    const int g = gt >> 3, j = gt & 7;
+    const uint64_t pol_x = policy_evict_last();
+    int r = 0; uint32_t rph = 0;
+    while (true) {
+      mbar_wait(&sfull[r], rph);
+      const int4 info = ring[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[r]);
+      if (++r == kRing) { r = 0; rph ^= 1; }
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      if (kind == kItemUp) {
+        const int row0 = info.z, nvalid = info.w;
+        int tok[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int rr = g + 8 * i;
+          tok[i] = rr < nvalid ? s_tok[row0 + rr] : -1;
+        }
+        const __nv_bfloat16* xs = p.x + j * 8;
+        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
+        for (int kb = 0; kb < p.H / kTileK; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          cp_async_wait_group<S_ - 1>();  // this slot's previous copies (S_ groups ago) landed
+          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + kATileBytes) + sw;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+            if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
+          cp_async_arrive_noinc(&bfull[stage]);
+          cp_async_commit();
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      } else {
+        for (int kb = 0; kb < p.I / kTileK; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive(&bfull[stage]);
+          cp_async_commit();
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // epilogue (w4-w7: TMEM lane quarter q = warp & 3), as k_experts_tiny
+    const int q = warp & 3;
+    const int et = tid - 128;  // 0..127
+    int r = 0; uint32_t rph = 0;
+    [[maybe_unused]] int n_item = 0;
+    int n_dn = 0;
+    while (true) {
+      mbar_wait(&sfull[r], rph);
+      const int4 info = ring[r];
+      const int kind = info.x & 0xff;
+      if (kind == kItemEnd) break;
+      const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      uint32_t v[16];
+      tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::kN, v);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == A_) { acc = 0; aph ^= 1; }
+      if (kind == kItemUp) {
+        named_bar_sync(2, 128);  // the previous item's readers are done with xbuf
+        if (q >= 2) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xbuf[i * 64 + 32 * (q - 2) + lane] = __uint_as_float(v[i]);
+        }
+        named_bar_sync(2, 128);
+        if (q < 2) {
+          const int feat = m0 + 32 * q + lane;
+          __nv_bfloat16* dst = p.act + static_cast<size_t>(row0) * p.I + feat;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < nvalid)
+              dst[static_cast<size_t>(i) * p.I] =
+                  __float2bfloat16_rn(silu_mul(__uint_as_float(v[i]), xbuf[i * 64 + 32 * q + lane]));
+        }
+        fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
+        named_bar_sync(1, 128);      // every thread's act stores precede the count
+      } else {
+        const int feat = m0 + 32 * q + lane;
+        if (feat < p.H) {
+          __nv_bfloat16* dst = p.y_perm + static_cast<size_t>(row0) * p.H + feat;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < nvalid) dst[static_cast<size_t>(i) * p.H] = __float2bfloat16_rn(__uint_as_float(v[i]));
+        }
+        if (p.y != nullptr) {
+          // Fused combine: per (token, 256-feature block) a counter of finished DN halves; the item
+          // completing a block (2 * topk halves) sums the token's topk y_perm rows over those 256
+          // features in fixed j order (bit-identical to k_combine) and writes y. Release: this
+          // item's y_perm stores precede the barrier and each row's acq_rel increment; acquire:
+          // the completing increment, then L2 reads (ld.cg) of the other items' rows.
+          int32_t* fin = s_fin + (n_dn & 1) * (C::kMaxT + 1);
+          ++n_dn;
+          if (et == 0) fin[C::kMaxT] = 0;  // readers of this buffer (two DN items ago) are past barrier 1
+          named_bar_sync(1, 128);
+          const int nfb = p.H / 256, fb = m0 / 256;
+          if (et < nvalid) {
+            const int t = s_tok[row0 + et];
+            uint32_t* c = p.cmb + t * nfb + fb;
+            if (atom_add_acqrel_gpu(c, 1u) == 2u * static_cast<uint32_t>(K) - 1u) {
+              *c = 0u;  // every increment of this call has happened: left zero for the next call
+              fin[atomicAdd(&fin[C::kMaxT], 1)] = t;
+            }
+          }
+          named_bar_sync(1, 128);
+          const int nfin = fin[C::kMaxT];
+          for (int i = q; i < nfin; i += 4) {
+            const int t = fin[i];
+            const size_t col = static_cast<size_t>(fb) * 256 + lane * 8;
+            float a8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] = 0.f;
+            for (int j0 = 0; j0 < K; j0 += 8) {  // eight rows in flight, summed in j order
+              uint4 d[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (j0 + u < K)
+                  d[u] = __ldcg(reinterpret_cast<const uint4*>(p.y_perm + static_cast<size_t>(s_slot[t * K + j0 + u]) *
+                                                                              p.H + col));
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                if (j0 + u < K) {
+                  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d[u]);
+                  const float wj = s_w[t * K + j0 + u];
+#pragma unroll
+                  for (int q2 = 0; q2 < 4; ++q2) {
+                    const float2 f = __bfloat1622float2(h2[q2]);
+                    a8[2 * q2] += wj * f.x;
+                    a8[2 * q2 + 1] += wj * f.y;
+                  }
+                }
+              }
+            }
+            uint4 o;
+            __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) o2[q2] = __floats2bfloat162_rn(a8[2 * q2], a8[2 * q2 + 1]);
+            *reinterpret_cast<uint4*>(p.y + static_cast<size_t>(t) * p.H + col) = o;
+          }
+        }
+      }
+      if (et == 0) {
+        mbar_arrive(&sempty[r]);
+        if (kind == kItemUp) {  // release: the item's act rows are written
+          __threadfence();
+          atomicAdd(&p.sched[1 + e], 1u);
+        }
+        LP_ITEM(n_item, 4, LP_NOW());
+      }
+      ++n_item;
+      if (++r == kRing) { r = 0; rph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {  // the last CTA out leaves the scheduler words zero for the next call
+    __threadfence();
+    if (atomicAdd(&p.sched[C::kExitWord], 1u) == gridDim.x - 1) {
+      for (int i = 0; i <= E; ++i) p.sched[i] = 0u;
+      p.sched[C::kExitWord] = 0u;
+      __threadfence();
+    }
+  }
+  if (tid == 0) LP_TRACE_MAX(53);
+  cluster_wait_acq();  // no CTA leaves while a cluster peer may still read its partials
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+}  // namespace lp

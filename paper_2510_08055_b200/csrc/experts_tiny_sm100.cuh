@@ -101,8 +101,11 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
       const uint64_t pol_a = policy_evict_last();
       int stage = 0; uint32_t phase = 0;
       int r = 0; uint32_t rph = 0;
+      [[maybe_unused]] int n_item = 0;
       while (true) {
         const int it = static_cast<int>(atomicAdd(&p.sched[0], 1u));  // every item claimed dynamically
+        LP_ITEM(n_item, 0, static_cast<unsigned long long>(it));
+        LP_ITEM(n_item, 1, LP_NOW());
         int4 info;
         int need = 0;
         if (it >= n_items) {
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
           while (ld_acquire_u32(&p.sched[1 + e]) < static_cast<uint32_t>(need)) __nanosleep(64);
           fence_proxy_async_global();
         }
+        LP_ITEM(n_item, 2, LP_NOW());
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
         const uint32_t bytes = kATileBytes + (up ? 0 : C::kBBytes);
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -153,6 +157,8 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
           }
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
+        LP_ITEM(n_item, 3, LP_NOW());
+        ++n_item;
       }
     }
     __syncwarp();
@@ -244,6 +250,7 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
     const int et = threadIdx.x - 128;  // 0..127
     int r = 0; uint32_t rph = 0;
     int acc = 0; uint32_t aph = 0;
+    [[maybe_unused]] int n_item = 0;
     while (true) {
       mbar_wait(&sfull[r], rph);
       const int4 info = ring[r];
@@ -291,7 +298,9 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
           __threadfence();
           atomicAdd(&p.sched[1 + e], 1u);
         }
+        LP_ITEM(n_item, 4, LP_NOW());
       }
+      ++n_item;
       if (++r == kRing) { r = 0; rph ^= 1; }
     }
   }

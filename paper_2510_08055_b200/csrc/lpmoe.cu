@@ -19,6 +19,7 @@
 #include "experts_sm100.cuh"
 #include "experts_pair_sm100.cuh"
 #include "experts_tiny_sm100.cuh"
+#include "decode_sm100.cuh"
 #include "ep_p2p.cuh"
 #include "norm.cuh"
 #include "permute.cuh"
@@ -97,8 +98,14 @@ int pick_max_n(int S, int E) {
 // every kernel leaves it zeroed again.
 constexpr int kMaxTokens = 262144;
 constexpr size_t kSchedOff = (kMaxTokens / 32) * 4;          // 32 KiB reserved (formerly router tickets)
-constexpr size_t kHeaderBytes = kSchedOff + 4096;            // + sched words (E+1 <= 257)
+constexpr size_t kHeaderBytes = kSchedOff + 8192;            // + sched words (E+1 <= 257), decode combine counters
 constexpr size_t kGbarOff = kSchedOff + 2048;                // fused router grid barrier (2 words)
+// k_decode's own scheduler words (item counter, per-expert UP counters, exit counter): only it
+// touches them and its last CTA leaves them zero (the other expert kernels leave `sched` dirty
+// until the next k_scan* resets it)
+constexpr size_t kDecodeSchedOff = kSchedOff + 2400;
+constexpr size_t kDecodeCmbOff = kSchedOff + 4096;  // k_decode's fused-combine counters (<= 1024 words)
+static_assert(kDecodeSchedOff + 4 * (lp::DecodeCfg::kExitWord + 1) <= kHeaderBytes, "decode scheduler words");
 
 struct Layout {
   size_t chunk_hist, rank_local, ids, w, counts, offsets, slot_of, tok_of;
@@ -567,6 +574,75 @@ int launch_experts_tiny(const void* x, const int32_t* tok_of, int S, const void*
   return LP_OK;
 }
 
+// Decode-size layers (T <= 16, T*topk <= E <= 128, H % 256 == 0) run router,
+// permutation and the expert stream in ONE launch (decode_sm100.cuh), bit-
+// identical to k_router<4, 4, 16> + k_scan_slots + k_experts_tiny. LPMOE_DECODE=0
+// disables; LPMOE_DECODE_W2_WARM=0 turns off its L2 warm-up of the hit experts' W2.
+bool use_decode(int T, int H, int I, int E, int topk) {
+  static const int v = env_int("LPMOE_DECODE", 1);
+  return v != 0 && T >= 1 && T <= lp::DecodeCfg::kMaxT && T * topk <= E && E <= lp::DecodeCfg::kMaxE &&
+         H % 256 == 0 && I % 64 == 0 && T * (H / 256) <= 1024;
+}
+
+int launch_decode(const void* x, const void* wr, const void* w13, const void* w2, int T, int H, int I, int E,
+                  int topk, int renorm, int32_t* ids, float* w, int32_t* counts, int32_t* offsets, int32_t* slot_of,
+                  int32_t* tok_of, void* act, void* y_perm, uint32_t* sched, void* y, uint32_t* cmb, int wpol,
+                  cudaStream_t st) {
+  static const int warm = env_int("LPMOE_DECODE_W2_WARM", 1);
+  int rc;
+  if ((rc = get_encode())) return rc;
+  const int S = T * topk;
+  CUtensorMap tm_wr, tm_x, tm_w13h, tm_w2, tm_act;
+  if ((rc = make_tmap(&tm_wr, wr, E, H, 128))) return rc;
+  if ((rc = make_tmap(&tm_x, x, T, H, lp::DecodeCfg::kN))) return rc;
+  if ((rc = make_tmap(&tm_w13h, w13, static_cast<uint64_t>(E) * 2 * I, H, 64))) return rc;
+  if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
+  if ((rc = make_tmap(&tm_act, act, S, I, lp::DecodeCfg::kN))) return rc;
+  constexpr int smem = lp::DecodeCfg::kSmemBytes;
+  static const int forced_cs = env_int("LPMOE_DECODE_CS", 0);
+  const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 4 ? 4 : 2);
+  auto kern = cs == 4 ? lp::k_decode<4> : lp::k_decode<2>;
+  if ((rc = set_smem(kern, smem))) return rc;
+  const lp::DecodeParams p{T, H, I, E, topk, renorm, static_cast<const __nv_bfloat16*>(x),
+                           static_cast<const uint8_t*>(w2), ids, w, counts, offsets, slot_of, tok_of,
+                           static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
+                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0};
+  // clusters of 4 that are co-resident (GPC boundaries can leave SMs that no 4-CTA cluster fits):
+  // a second wave would repeat the routing prologue after the first wave's stream
+  static std::mutex mu;
+  static int cached[64][2] = {};
+  int dev = 0;
+  LP_CUDA(cudaGetDevice(&dev));
+  int grid;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    int& g = cached[dev & 63][cs == 4];
+    if (g <= 0) {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(sm_count() / cs * cs);
+      cfg.blockDim = dim3(lp::DecodeCfg::kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = sm_count() / cs;
+      }
+      g = n * cs;
+    }
+    grid = g;
+  }
+  LP_CUDA(launch_pdl_cluster(kern, grid, lp::DecodeCfg::kThreads, smem, st, cs, tm_wr, tm_x, tm_w13h, tm_w2, tm_act,
+                             p));
+  return LP_OK;
+}
+
 // k-blocks of the first item's W13 warmed in L2 before pdl_wait (2 x 16 KiB each);
 // tuning knob LPMOE_PREFETCH_KB (default 32 = the whole first UP item, 1 MiB per CTA;
 // B200, T=576: 210.4-211.5 vs 211.8-212.2 us at 16, e2e 208 vs 210.5).
@@ -831,6 +907,21 @@ int lp_moe_forward(const void* x, const void* wr, const void* w13, const void* w
   const bool gather = tiny || use_gather(max_n);
   const bool fused = use_fused_combine();
   const bool fused_route = !fused && fused_route_ok(L, T, E);
+  if (!fused && !fused_route && use_decode(T, H, I, E, topk)) {  // one launch + combine
+    prof_mark(0, st);
+    prof_mark(1, st);
+    prof_mark(2, st);
+    // the combine runs inside k_decode's DN epilogues unless LPMOE_DECODE_COMBINE=0
+    static const bool fuse_combine = env_int("LPMOE_DECODE_COMBINE", 1) != 0;
+    if ((rc = launch_decode(x, wr, w13, w2, T, H, I, E, topk, renorm, ids, w, counts, offsets, slot_of, tok_of,
+                            at<void>(ws, L.act), at<void>(ws, L.y_perm), at<uint32_t>(ws, kDecodeSchedOff),
+                            fuse_combine ? y : nullptr, at<uint32_t>(ws, kDecodeCmbOff), env_wpol(), st)))
+      return rc;
+    prof_mark(3, st);
+    if (!fuse_combine && (rc = lp_moe_combine(at<void>(ws, L.y_perm), slot_of, w, T, H, topk, y, stream))) return rc;
+    prof_mark(4, st);
+    return ok();
+  }
   const size_t warm = l2_warm_bytes(static_cast<size_t>(E) * 2 * I * H * 2);
   prof_mark(0, st);
   if (fused_route) {  // router + grid barrier + permutation in one launch
@@ -1048,9 +1139,17 @@ int lp_trace_fetch(unsigned long long* out, int n) {
   if (cudaMemcpyFromSymbol(out, lp::g_lp_trace, sizeof(unsigned long long) * n) != cudaSuccess) return LP_ECUDA;
   return LP_OK;
 }
+int lp_trace_items(unsigned long long* out, int n) {
+  const int total = lp::kTraceCtas * lp::kTraceItems * lp::kTraceFields;
+  if (n > total) n = total;
+  if (cudaMemcpyFromSymbol(out, lp::g_lp_items, sizeof(unsigned long long) * n) != cudaSuccess) return LP_ECUDA;
+  return LP_OK;
+}
 int lp_trace_reset(void) {
+  static unsigned long long zeros[lp::kTraceCtas * lp::kTraceItems * lp::kTraceFields] = {};
+  if (cudaMemcpyToSymbol(lp::g_lp_items, zeros, sizeof(zeros)) != cudaSuccess) return LP_ECUDA;
   unsigned long long init[512];
-  for (int i = 0; i < 512; ++i) init[i] = (i % 8 == 0 || i == 24 || i == 32 || i == 40) ? ~0ull : 0ull;
+  for (int i = 0; i < 512; ++i) init[i] = (i % 8 == 0 || i == 24 || i == 32 || i == 40 || i == 52) ? ~0ull : 0ull;
   if (cudaMemcpyToSymbol(lp::g_lp_trace, init, sizeof(init)) != cudaSuccess) return LP_ECUDA;
   return LP_OK;
 }

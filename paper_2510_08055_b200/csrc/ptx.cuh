@@ -306,10 +306,26 @@ __device__ __forceinline__ void lp_trace_max(int slot) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   atomicMax(&g_lp_trace[slot], t);
 }
+// per-CTA work-item timeline of the decode-size expert kernel: [cta][item][field]
+// fields: 0 item id, 1 claimed, 2 dependency met (DN) / claimed (UP), 3 last TMA issued, 4 epilogue done
+constexpr int kTraceCtas = 160, kTraceItems = 8, kTraceFields = 5;
+__device__ unsigned long long g_lp_items[kTraceCtas * kTraceItems * kTraceFields];
+__device__ __forceinline__ unsigned long long lp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void lp_item(int n, int field, unsigned long long v) {
+  if (blockIdx.x < kTraceCtas && n < kTraceItems) g_lp_items[(blockIdx.x * kTraceItems + n) * kTraceFields + field] = v;
+}
+#define LP_ITEM(n, field, v) lp_item(n, field, v)
+#define LP_NOW() lp_now()
 #define LP_TRACE_AT(cond, slot) do { if (cond) lp_trace(slot); } while (0)
 #define LP_TRACE_MIN(slot) lp_trace_min(slot)
 #define LP_TRACE_MAX(slot) lp_trace_max(slot)
 #else
+#define LP_ITEM(n, field, v) do { } while (0)
+#define LP_NOW() 0ull
 #define LP_TRACE_AT(cond, slot) do { } while (0)
 #define LP_TRACE_MIN(slot) do { } while (0)
 #define LP_TRACE_MAX(slot) do { } while (0)

@@ -314,12 +314,16 @@ class PeerEP:
         sl = slice(rank * el, (rank + 1) * el)
         return cls(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, max_tokens, group, region)
 
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, EPStats]:
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, prof=None) -> tuple[torch.Tensor, EPStats]:
+        """prof: optional list of 5 CUDA events recorded at the stage boundaries (start | route +
+        permute | counts + dispatch | experts | combine) for bench.py's per-rank stage split."""
         s, P, el, lib, rg = self.shape, self.world, self.el, self.lib, self.region
+        mark = (lambda i: prof[i].record()) if prof is not None else (lambda i: None)
         require(x.dim() == 2 and x.shape[1] == s.hidden, f"x must be [T, {s.hidden}], got {tuple(x.shape)}")
         T, H, k = x.shape[0], s.hidden, s.top_k
         require(T <= self.max_tokens, f"T={T} exceeds max_tokens={self.max_tokens}")
         st = _stream_ptr(self.device)
+        mark(0)
         ids, w = self.ops.route(x, self.wr, k, s.norm_topk_prob)
         counts = torch.zeros((s.num_experts,), dtype=torch.int32, device=self.device)
         offsets = torch.zeros((s.num_experts + 1,), dtype=torch.int32, device=self.device)
@@ -331,6 +335,7 @@ class PeerEP:
             _native.check(lib.lp_moe_permute(ids.data_ptr(), x.data_ptr(), T, H, s.num_experts, k, counts.data_ptr(),
                                              offsets.data_ptr(), slot_of.data_ptr(), tok_of.data_ptr(), None,
                                              ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
+        mark(1)
         _native.check(lib.lp_ep_post_counts(counts.data_ptr(), rg.peer_inbox.data_ptr(), P, el, self.rank, st),
                       "lp_ep_post_counts")
         rg.barrier(st)
@@ -342,6 +347,7 @@ class PeerEP:
                                          rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(), T, H, k, el,
                                          dest_rank.data_ptr(), dest_row.data_ptr(), st), "lp_ep_dispatch")
         rg.barrier(st)
+        mark(2)
         # rows received stay on the device (off_local[El]): capacity-sized launch, tile width from the
         # expected T*k rows; no host sync, so the whole layer is stream-ordered and graph-capturable
         act = rg.act(s.ffn)
@@ -351,10 +357,12 @@ class PeerEP:
                                               act.data_ptr(), rg.y_out_ptr, ws.data_ptr(), ws.numel(), st),
                       "lp_moe_experts_rows")
         rg.barrier(st)
+        mark(3)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
         _native.check(lib.lp_ep_combine(rg.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
                                         w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
         rg.barrier(st)
+        mark(4)
         self.last_ids, self.last_weights = ids, w
         # recv_rows: a stream-ordered copy (the region's off_local is rewritten by the next layer)
         return y, EPStats(counts, rg.off_local[el].clone(), counts.view(P, el).sum(1), [], s)

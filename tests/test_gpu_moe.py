@@ -183,9 +183,10 @@ def test_permute_slot_maps_without_rows(cuda, T):
     np.testing.assert_array_equal(tok_of.cpu().numpy(), rt)
 
 
-@pytest.mark.parametrize("T,launches", [(1, 4), (576, 4), (4100, 5)])
+@pytest.mark.parametrize("T,launches", [(1, 1), (16, 1), (17, 4), (576, 4), (4100, 5)])
 def test_forward_launch_count(cuda, T, launches):
-    """One layer = router, scan+slots (or scan, scatter), expert kernel, combine: counted by liblpmoe."""
+    """One layer = router, scan+slots (or scan, scatter), expert kernel, combine; decode-size
+    batches (T <= 16, T*k <= E) = ONE launch (k_decode, combine fused): counted by liblpmoe."""
     s = QWEN3_30B_A3B
     _, _, _, layer = make(s, 21, cuda)
     x = router_tokens(T, s.hidden, 7).to(cuda)
@@ -302,7 +303,8 @@ def test_host_pipeline_matches_device_forward(cuda):
 
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
                                   "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0",
-                                  "LPMOE_SCAN_SLOTS=0"])
+                                  "LPMOE_SCAN_SLOTS=0", "LPMOE_DECODE=0", "LPMOE_DECODE_W2_WARM=0",
+                                  "LPMOE_DECODE_COMBINE=0", "LPMOE_DECODE_CS=2", "LPMOE_DECODE_CS=4"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
@@ -346,7 +348,7 @@ def test_back_to_back_layers_large_T(cuda):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("T", [576, 4100])
+@pytest.mark.parametrize("T", [1, 576, 4100])
 def test_cuda_graph_capture_replays_layer(cuda, T):
     """lpmoe.h promises a graph-capturable layer (no host sync, no allocation, PDL and cluster
     launches inside): capture once, replay on new inputs, compare with eager calls bit for bit."""
@@ -371,3 +373,73 @@ def test_cuda_graph_capture_replays_layer(cuda, T):
         ref, _ = layer(x)
         torch.cuda.synchronize()
         assert torch.equal(y_static, ref)
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 5, 16])
+def test_decode_kernel_matches_oracle(cuda, T):
+    """The fused decode-size kernel (router + permutation + experts in one launch, T <= 16):
+    ids / counts / offsets / slots bit-exact, weights to rtol 2e-5, output rel-L2 <= 1e-2."""
+    s = QWEN3_30B_A3B
+    err, stats, ref = check_layer(s, T, 41, cuda)
+    assert stats.experts_hit == len(np.unique(ref["ids"]))
+
+
+def test_decode_kernel_bit_identical_to_staged_path(cuda):
+    """k_decode reproduces k_router<4,4,16> + k_scan_slots + k_experts_tiny + k_combine bit for bit:
+    the same token batch through LPMOE_DECODE=0 (subprocess) gives identical ids, weights and rows,
+    on dyadic and Gaussian inputs, with norm_topk_prob on and off (tiny config)."""
+    import subprocess
+    import sys
+
+    code = "\n".join([
+        "import sys; sys.path[:0] = ['.', 'tests']",
+        "import torch, numpy as np",
+        "from test_gpu_moe import make",
+        "from paper_2510_08055_b200 import QWEN3_30B_A3B, MoEShape",
+        "from paper_2510_08055_b200.synthetic import router_tokens",
+        "d = torch.device('cuda', 0); out = {}; g = torch.Generator().manual_seed(5)",
+        "for si, s in enumerate([QWEN3_30B_A3B, MoEShape(256, 128, 16, 2, False)]):",
+        "    layer = make(s, 81, d)[3]",
+        "    for T in (1, 4, 8):",
+        "        for kind in ('dy', 'gs'):",
+        "            x = router_tokens(T, s.hidden, 90 + T) if kind == 'dy' else "
+        "torch.randn((T, s.hidden), generator=g).to(torch.bfloat16)",
+        "            y, st = layer(x.to(d)); torch.cuda.synchronize()",
+        "            k = f'{si}_{T}_{kind}'",
+        "            out[k + '_y'] = y.float().cpu().numpy(); out[k + '_ids'] = layer.last_ids.cpu().numpy()",
+        "            out[k + '_w'] = layer.last_weights.cpu().numpy(); out[k + '_c'] = st.counts.cpu().numpy()",
+        "np.savez(sys.argv[1], **out); print('ok')",
+    ])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+
+    res = []
+    with tempfile.TemporaryDirectory() as td:
+        for flag in ("1", "0"):
+            path = os.path.join(td, f"d{flag}.npz")
+            env = dict(os.environ, LPMOE_DECODE=flag)
+            r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+            res.append(dict(np.load(path)))
+    a, b = res
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_decode_kernel_back_to_back_and_mixed_sizes(cuda):
+    """Scheduler words are left zero by the last CTA out: decode layers chained without a host sync,
+    interleaved with larger batches on the same workspace, keep giving the first call's result."""
+    s = QWEN3_30B_A3B
+    layer = make(s, 21, cuda)[3]
+    xs = {T: router_tokens(T, s.hidden, 200 + T).to(cuda) for T in (1, 8, 16, 64, 576)}
+    ref = {T: layer(x)[0].clone() for T, x in xs.items()}
+    torch.cuda.synchronize()
+    outs = []
+    for i in range(40):
+        T = (1, 8, 64, 16, 1, 576)[i % 6]
+        outs.append((T, layer(xs[T])[0].clone()))
+    torch.cuda.synchronize()
+    for T, y in outs:
+        assert torch.equal(y, ref[T]), T
