@@ -126,7 +126,9 @@ class ClockSampler:
         mx = [num(r[2]) for r in win if len(r) > 2 and num(r[2]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in win if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
+        pw = [num(r[3]) for r in win if len(r) > 3 and num(r[3]) is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w": statistics.median(pw) if pw else None, "power_max_w": max(pw) if pw else None,
                 "reasons": reasons, "samples": len(win), "window": window}
 
 

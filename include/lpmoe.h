@@ -147,21 +147,27 @@ int lp_ipc_free(void* dptr);
 int lp_ipc_open(const void* handle64, void** dptr);
 int lp_ipc_close(void* dptr);
 
-/* Device-side barrier over P ranks: adds 1 to every rank's uint32 counter
- * (system-scope release), then waits until peer_flag[rank] reaches `target`
- * (= P x number of barriers so far, counters only grow). */
-int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, void* stream);
+/* Bytes of a rank's EP control block (the first bytes of its zero-filled
+ * region, 256-aligned by the caller): u32 barrier counter, u32 barrier and
+ * layer sequence numbers, ready tags [2][32], int32 count inbox [2][P][E].
+ * 0 when P > 32 or E is not a multiple of P. */
+size_t lp_ep_ctl_bytes(int P, int E);
 
-/* inbox_d[rank*El + el] = counts[d*El + el] for every rank d (counts: this
- * rank's per-global-expert routing counts, int32 [P*El]). */
-int lp_ep_post_counts(const int32_t* counts, int32_t* const* peer_inbox, int P, int El, int rank, void* stream);
+/* Device-side barrier over P ranks: adds 1 to every rank's counter
+ * (system-scope release), then waits until its own counter reaches P x the
+ * number of barriers it has passed (kept in its control block, so captured
+ * CUDA graphs replay correctly). peer_ctl: device array of the P control blocks. */
+int lp_ep_barrier(uint32_t* const* peer_ctl, int P, int rank, void* stream);
 
-/* After the barrier that follows post_counts: dest_base[d*El+el] = first row
- * of this rank's entries for expert el in rank d's receive buffer (rows
- * expert-major, source-rank-major within an expert); off_local[0..El] = this
- * rank's expert offsets over all sources (off_local[El] = rows received). */
-int lp_ep_plan(int32_t* const* peer_inbox, int P, int El, int rank, int32_t* dest_base, int32_t* off_local,
-               void* stream);
+/* Count exchange + plan (one launch, replaces a post / barrier / plan
+ * sequence): this rank's per-global-expert counts (int32 [P*El]) go to every
+ * rank's inbox, followed by a system-scope ready tag; once every source's tag
+ * is in this rank's block: dest_base[d*El+el] = first row of this rank's
+ * entries for expert el in rank d's receive buffer (rows expert-major,
+ * source-rank-major within an expert); off_local[0..El] = this rank's expert
+ * offsets over all sources (off_local[El] = rows received). */
+int lp_ep_exchange(const int32_t* counts, uint32_t* const* peer_ctl, int P, int El, int rank, int32_t* dest_base,
+                   int32_t* off_local, void* stream);
 
 /* Fused permute + dispatch: entry i = t*topk + j (ids/slot_of/offsets from
  * lp_moe_route + lp_moe_permute over the P*El global experts) stores x[t]

@@ -11,22 +11,25 @@ from __future__ import annotations
 import numpy as np
 
 
-def post_counts(counts: np.ndarray, inboxes: list, P: int, El: int, rank: int) -> None:
-    """k_ep_post_counts: inbox_d[rank * El + el] = counts[d * El + el] for every rank d."""
-    for d in range(P):
-        inboxes[d][rank * El:(rank + 1) * El] = counts[d * El:(d + 1) * El]
+def post_counts(counts: np.ndarray, inboxes: list, rank: int, layer: int) -> None:
+    """k_ep_exchange, first half: inbox_d[layer & 1][rank][:] = counts (this rank's per-global-expert
+    counts) for every rank d; the GPU follows it with a system-scope ready tag = layer + 1, which
+    the callers here replace with a barrier."""
+    for box in inboxes:
+        box[layer & 1, rank, :] = counts
 
 
-def plan(inboxes: list, P: int, El: int, rank: int):
-    """k_ep_plan: -> dest_base [P*El] (this rank's first row per (owner d, expert el) in d's
-    receive buffer; rows expert-major, source-rank-major within an expert) and off_local [El+1]
-    (this rank's expert offsets over all sources)."""
-    cnt = np.stack([np.asarray(inboxes[d]).reshape(P, El) for d in range(P)])  # [dest, src, el]
+def plan(inbox: np.ndarray, P: int, El: int, rank: int, layer: int):
+    """k_ep_exchange, second half, from this rank's OWN inbox [2][P src][E] once every source posted:
+    -> dest_base [P*El] (this rank's first row per (owner d, expert el) in d's receive buffer; rows
+    expert-major, source-rank-major within an expert) and off_local [El+1] (this rank's expert
+    offsets over all sources)."""
+    cnt = np.asarray(inbox[layer & 1]).reshape(P, P, El)  # [src, dest, el]
     dest_base = np.zeros(P * El, np.int64)
     for d in range(P):
         for el in range(El):
-            dest_base[d * El + el] = cnt[d, :, :el].sum() + cnt[d, :rank, el].sum()
-    per_expert = cnt[rank].sum(axis=0)  # rows rank receives per local expert
+            dest_base[d * El + el] = cnt[:, d, :el].sum() + cnt[:rank, d, el].sum()
+    per_expert = cnt[:, rank, :].sum(axis=0)  # rows rank receives per local expert
     off_local = np.zeros(El + 1, np.int64)
     np.cumsum(per_expert, out=off_local[1:])
     return dest_base, off_local

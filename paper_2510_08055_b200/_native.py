@@ -47,9 +47,9 @@ SIGNATURES = {
     "lp_ipc_alloc": (_i, [_sz, _p]),
     "lp_ipc_free": (_i, [_p]),
     "lp_ipc_close": (_i, [_p]),
-    "lp_ep_barrier": (_i, [_p, _i, _i, ctypes.c_uint32, _p]),
-    "lp_ep_post_counts": (_i, [_p, _p, _i, _i, _i, _p]),
-    "lp_ep_plan": (_i, [_p, _i, _i, _i, _p, _p, _p]),
+    "lp_ep_ctl_bytes": (_sz, [_i, _i]),
+    "lp_ep_barrier": (_i, [_p, _i, _i, _p]),
+    "lp_ep_exchange": (_i, [_p, _p, _i, _i, _i, _p, _p, _p]),
     "lp_ep_dispatch": (_i, [_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _p, _p, _p]),
     "lp_ep_combine": (_i, [_p, _p, _p, _p, _i, _i, _i, _p, _p]),
 }

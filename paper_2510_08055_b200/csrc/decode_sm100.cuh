@@ -69,6 +69,7 @@ struct DecodeCfg {
   static_assert(kLogitBytes + kTopBytes <= kStageBytes, "routing scratch fits one ring stage");
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kXBytes + kPartBytes + kPermBytes + kBarBytes;
   static constexpr int kExitWord = 1 + kMaxExperts + 8;  // sched word counting finished CTAs
+  static constexpr int kUpDoneWord = 1 + kMaxExperts + 4;  // UP items finished (all experts)
 };
 static_assert(DecodeCfg::kSmemBytes <= 232448, "decode kernel shared memory");
 static_assert(DecodeCfg::kPermBytes % 16 == 0, "barrier / ring alignment");
@@ -88,11 +89,13 @@ struct DecodeParams {
   int32_t* tok_of;         // [T*topk]
   __nv_bfloat16* act;      // [S, I]
   __nv_bfloat16* y_perm;   // [S, H]
-  uint32_t* sched;         // [0] item counter, [1+e] UP items done, [kExitWord] finished CTAs
+  uint32_t* sched;         // [0] item counter, [1+e] UP items done, [kUpDoneWord] all UP items done,
+                           // [kExitWord] finished CTAs
   __nv_bfloat16* y;        // [T, H] combined output (nullptr: the caller runs k_combine)
   uint32_t* cmb;           // [T * H/256] fused-combine counters, zero on entry and left zero
   int weights_evict_first;
   int warm_w2;             // 1: L2-prefetch the hit experts' W2 when small
+  int dnc;                 // 1: block-diagonal DN + combine items when S <= 16 and every UP item fits one wave
 };
 
 __device__ __forceinline__ void cluster_arrive_rel() {
@@ -111,7 +114,9 @@ template <int CS>
 __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     k_decode(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const __grid_constant__ CUtensorMap tm_w13h, const __grid_constant__ CUtensorMap tm_w2,
-             const __grid_constant__ CUtensorMap tm_act, const DecodeParams p) {
+             const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w2r8,
+             const __grid_constant__ CUtensorMap tm_w2r16, const __grid_constant__ CUtensorMap tm_w2r32,
+             const __grid_constant__ CUtensorMap tm_w2r64, const DecodeParams p) {
   using C = DecodeCfg;
   constexpr int kCl = CS;                 // CTAs per cluster
   constexpr int kPpc = C::kParts / CS;    // partial sums per CTA
@@ -359,7 +364,18 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
   const int mt_up = p.I / 64;
   const int mt_dn = (p.H + kTileM - 1) / kTileM;
   const int n_up = mt_up * nnz;
-  const int n_items = (mt_up + mt_dn) * nnz;
+  // S <= 16 (T <= 2 at top-8): DN items are block-diagonal tiles of ALL hit experts — rows
+  // [j*R, (j+1)*R) of the 128-row A tile are W2 rows f0..f0+R-1 of hit expert j (R = 128 / nnz
+  // rounded up to a power of two), B = every slot's act row, so D[j*R + r][slot] is expert j's
+  // output feature f0 + r for that slot (the other columns are discarded). Each item then holds
+  // every routed row of its R features and combines them in the epilogue (fixed j order, the
+  // bf16-rounded row values: bit-identical to k_combine) — no y_perm round trip, no cross-CTA
+  // completion counters on the critical path.
+  // (all UP items must run in one wave: a DNC item waits for EVERY UP item, not just its expert's)
+  const bool dnc = p.dnc && p.y != nullptr && S <= C::kN && n_up <= static_cast<int>(gridDim.x);
+  int rdnc = 128;
+  while (dnc && rdnc > 8 && rdnc * nnz > 128) rdnc >>= 1;
+  const int n_items = n_up + (dnc ? p.H / rdnc : mt_dn * nnz);
 
   // =============================== expert stream (k_experts_tiny's pipeline) ===============================
   if (warp == 0) {
@@ -385,7 +401,10 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
       int r = 0; uint32_t rph = 0;
       [[maybe_unused]] int n_item = 0;
       while (true) {
-        const int it = static_cast<int>(atomicAdd(&p.sched[0], 1u));  // every item claimed dynamically
+        // first item static (CTA b takes item b: no global atomic round trip before the first weight load),
+        // the rest claimed dynamically in item order (all UP items precede all DN items: deadlock-free)
+        const int it = n_item == 0 ? static_cast<int>(blockIdx.x)
+                                   : static_cast<int>(gridDim.x + atomicAdd(&p.sched[0], 1u));
         if (n_item == 0) LP_TRACE_MIN(52);
         LP_ITEM(n_item, 0, static_cast<unsigned long long>(it));
         LP_ITEM(n_item, 1, LP_NOW());
@@ -394,11 +413,15 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
           info = make_int4(kItemEnd, 0, 0, 0);
         } else {
           const bool up = it < n_up;
-          const int mtc = up ? mt_up : mt_dn;
-          const int local = up ? it : it - n_up;
-          const int e = s_hit[local / mtc];
-          const int mt = local % mtc;
-          info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * (up ? 64 : kTileM), s_off[e], s_cnt[e]);
+          if (!up && dnc) {
+            info = make_int4(kItemDnc, (it - n_up) * rdnc, 0, S);
+          } else {
+            const int mtc = up ? mt_up : mt_dn;
+            const int local = up ? it : it - n_up;
+            const int e = s_hit[local / mtc];
+            const int mt = local % mtc;
+            info = make_int4((up ? kItemUp : kItemDown) | (e << 8), mt * (up ? 64 : kTileM), s_off[e], s_cnt[e]);
+          }
         }
         mbar_wait(&sempty[r], rph ^ 1);
         ring[r] = info;
@@ -417,6 +440,41 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
             tma_load_2d(sa, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + m0, pol_w);
             tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + p.I + m0, pol_w);
             if (++stage == S_) { stage = 0; phase ^= 1; }
+          }
+        } else if (kind == kItemDnc) {
+          // W2 rows f0..f0+R-1 of every hit expert first, then all slots' act rows once every UP item is done
+          const CUtensorMap* tmr = rdnc == 8 ? &tm_w2r8 : rdnc == 16 ? &tm_w2r16 : rdnc == 32 ? &tm_w2r32
+                                   : rdnc == 64 ? &tm_w2r64 : &tm_w2;
+          const uint32_t abytes = static_cast<uint32_t>(nnz * rdnc * 128);
+          const int kblocks = p.I / kTileK;
+          const int npre = kblocks < S_ ? kblocks : S_;
+          const int st0 = stage;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            if (kb == npre) {
+              while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
+              fence_proxy_async_global();
+              LP_ITEM(n_item, 2, LP_NOW());
+              for (int k2 = 0, s2 = st0; k2 < npre; ++k2) {
+                tma_load_2d(smem + s2 * C::kStageBytes + kATileBytes, &tm_act, &full[s2], k2 * kTileK, 0, pol_a);
+                if (++s2 == S_) s2 = 0;
+              }
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::kStageBytes;
+            mbar_arrive_expect_tx(&full[stage], abytes + C::kBBytes);
+            for (int j = 0; j < nnz; ++j)
+              tma_load_2d(sa + j * rdnc * 128, tmr, &full[stage], kb * kTileK, s_hit[j] * p.H + m0, pol_w);
+            if (kb >= npre) tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, 0, pol_a);
+            if (++stage == S_) { stage = 0; phase ^= 1; }
+          }
+          if (npre == kblocks) {  // every k-block fitted the ring: the act rows follow the dependency
+            while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
+            fence_proxy_async_global();
+            LP_ITEM(n_item, 2, LP_NOW());
+            for (int k2 = 0, s2 = st0; k2 < npre; ++k2) {
+              tma_load_2d(smem + s2 * C::kStageBytes + kATileBytes, &tm_act, &full[s2], k2 * kTileK, 0, pol_a);
+              if (++s2 == S_) s2 = 0;
+            }
           }
         } else {
           // W2 tiles first (they do not depend on the UP items), the act rows once expert e's act is final
@@ -453,6 +511,7 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       int r = 0; uint32_t rph = 0;
+      [[maybe_unused]] int n_item = 0;
       while (true) {
         mbar_wait(&sfull[r], rph);
         const int4 info = ring[r];
@@ -470,6 +529,9 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
           mbar_wait(&full[stage], phase);
           mbar_wait(&bfull[stage], phase);
           tc_fence_after();
+          if (kb == 0) LP_ITEM(n_item, 5, LP_NOW());
+          if (kb == kblocks - 2) LP_ITEM(n_item, 8, LP_NOW());
+          if (kb == kblocks - 1) LP_ITEM(n_item, 9, LP_NOW());
           const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
           const uint64_t a0 = sdesc_kmajor_sw128(sa);
           const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
@@ -479,6 +541,8 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
+        LP_ITEM(n_item, 6, LP_NOW());
+        ++n_item;
         if (++acc == A_) { acc = 0; aph ^= 1; }
       }
     }
@@ -543,6 +607,7 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
       const int e = info.x >> 8, m0 = info.y, row0 = info.z, nvalid = info.w;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (et == 0) LP_ITEM(n_item, 7, LP_NOW());
       uint32_t v[16];
       tmem_ld16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::kN, v);
       tmem_wait_ld();
@@ -567,6 +632,26 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
         }
         fence_proxy_async_global();  // act rows are read back through TMA (async proxy)
         named_bar_sync(1, 128);      // every thread's act stores precede the count
+      } else if (kind == kItemDnc) {
+        // lane m = j*R + r of the block-diagonal tile: expert slot j (hit expert s_hit[j]), feature m0 + r
+        __nv_bfloat16* yv = reinterpret_cast<__nv_bfloat16*>(xbuf);  // [S slots][R] bf16 row values
+        named_bar_sync(2, 128);  // the previous item's readers are done with xbuf
+        const int jx = et / rdnc, r = et - jx * rdnc;
+        if (jx < nnz) {
+          const int e = s_hit[jx];
+          const int n0 = s_off[e], n1 = n0 + s_cnt[e];
+#pragma unroll
+          for (int n = 0; n < 16; ++n)
+            if (n >= n0 && n < n1) yv[n * rdnc + r] = __float2bfloat16_rn(__uint_as_float(v[n]));
+        }
+        named_bar_sync(2, 128);
+        for (int idx = et; idx < T * rdnc; idx += 128) {
+          const int t = idx / rdnc, rr = idx - t * rdnc;
+          float a = 0.f;
+          for (int jj = 0; jj < K; ++jj)  // fixed j order, as k_combine
+            a += s_w[t * K + jj] * __bfloat162float(yv[s_slot[t * K + jj] * rdnc + rr]);
+          p.y[static_cast<size_t>(t) * p.H + m0 + rr] = __float2bfloat16_rn(a);
+        }
       } else {
         const int feat = m0 + 32 * q + lane;
         if (feat < p.H) {
@@ -636,6 +721,7 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
         if (kind == kItemUp) {  // release: the item's act rows are written
           __threadfence();
           atomicAdd(&p.sched[1 + e], 1u);
+          if (dnc) atomicAdd(&p.sched[C::kUpDoneWord], 1u);
         }
         LP_ITEM(n_item, 4, LP_NOW());
       }
@@ -649,6 +735,7 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     __threadfence();
     if (atomicAdd(&p.sched[C::kExitWord], 1u) == gridDim.x - 1) {
       for (int i = 0; i <= E; ++i) p.sched[i] = 0u;
+      p.sched[C::kUpDoneWord] = 0u;
       p.sched[C::kExitWord] = 0u;
       __threadfence();
     }

@@ -2,25 +2,30 @@
 // mappings): the dispatch and return all-to-alls of ep.py's NCCL path folded
 // into the permutation and the combine.
 //
-// Every rank exposes, at the same logical layout, an inbox of per-source
-// expert counts, a receive buffer recv_x [cap, H] and its expert outputs
-// y_out [cap, H]; the other ranks hold mapped pointers to them (device arrays
-// of P pointers). Per layer, rank r (P ranks, E = P * El experts):
+// Every rank exposes, at the same logical layout, a control block (barrier
+// counter, double-buffered count inbox + ready tags), a receive buffer
+// recv_x [cap, H] and its expert outputs y_out [cap, H]; the other ranks hold
+// mapped pointers to them (device arrays of P pointers). Per layer, rank r
+// (P ranks, E = P * El experts), 6 launches after route + permute:
 //   1. route + local slot order (liblpmoe route / permute, index-only)
-//   2. k_ep_post_counts: counts of r's tokens per expert of rank d -> inbox_d[r]
-//   3. barrier
-//   4. k_ep_plan: from every destination's inbox, r's first row in d's receive
-//      buffer per expert (rows are expert-major, source-major within an expert,
-//      source order within a source: the layout a single-GPU x_perm of the
-//      concatenated batch would have per expert), and r's own expert offsets
-//   5. k_ep_dispatch: token rows stored straight into the owners' recv_x
+//   2. k_ep_exchange: r's counts -> every rank's inbox, release a ready tag,
+//      wait for every source's tag in r's own block, then plan: r's first row
+//      in each owner's receive buffer per expert (rows are expert-major,
+//      source-major within an expert, source order within a source: the
+//      layout a single-GPU x_perm of the concatenated batch would have per
+//      expert), and r's own expert offsets
+//   3. k_ep_dispatch: token rows stored straight into the owners' recv_x
 //      (fused permute + send, no staging buffer)
-//   6. barrier; owners run the expert kernel on recv_x -> y_out
-//   7. barrier; k_ep_combine: y[t] = sum_j w[t,j] * y_out_d[row] read straight
+//   4. barrier; owners run the expert kernel on recv_x -> y_out
+//   5. barrier; k_ep_combine: y[t] = sum_j w[t,j] * y_out_d[row] read straight
 //      from the owners (fused receive + weighted combine, fixed j order)
-//   8. barrier (buffers reusable)
-// Barriers are device-side: each rank adds 1 to every rank's counter with a
-// system-scope release and spins on its own with a system-scope acquire.
+// No end-of-layer barrier: a source writes an owner's recv_x again only after
+// the next layer's exchange saw the owner's tag (posted after its expert
+// kernel), and an owner rewrites y_out only after the next dispatch barrier
+// (every source has finished its combine). Barriers are device-side: each rank
+// adds 1 to every rank's counter with a system-scope release and spins on its
+// own with a system-scope acquire; the barrier and layer sequence numbers live
+// in device memory, so a layer is CUDA-graph capturable.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -36,60 +41,88 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
   return v;
 }
 
-// One warp: signal every rank, then wait until this rank's counter reaches
-// `target` (= P * barrier epoch). Counters only grow.
-__global__ void k_ep_barrier(uint32_t* const* __restrict__ peer_flag, int P, int rank, uint32_t target) {
+// Per-rank control block (the first lp_ep_ctl_bytes(P, E) bytes of a rank's region):
+//   u32 [0]  barrier counter (peers add to it)      u32 [1]  barriers this rank passed (own)
+//   u32 [2]  layers this rank exchanged (own)       u32 [64 + 2*parity + ...] ready tags, [2][P]
+//   int32 inbox [2][P src][E] at byte kCtlInbox      (parity = layer & 1: double-buffered)
+constexpr int kCtlReadyWord = 64;
+constexpr int kCtlInbox = 512;
+constexpr int kEpMaxRanks = 32;
+
+// One warp: signal every rank, then wait until this rank's counter reaches P x (barriers so
+// far, kept on the device in ctl[1], so a captured CUDA graph replays correctly). Counters only
+// grow; no rank can arrive at barrier n+1 before every rank arrived at barrier n.
+__global__ void k_ep_barrier(uint32_t* const* __restrict__ peer_ctl, int P, int rank) {
   const int lane = threadIdx.x;
+  uint32_t* mine = peer_ctl[rank];
   __threadfence_system();
   __syncwarp();
-  for (int q = lane; q < P; q += 32) red_add_release_sys(peer_flag[q], 1u);
+  for (int q = lane; q < P; q += 32) red_add_release_sys(peer_ctl[q], 1u);
   if (lane == 0) {
-    const uint32_t* mine = peer_flag[rank];
-    while (static_cast<int32_t>(ld_acquire_sys(mine) - target) < 0) __nanosleep(128);
+    const uint32_t n = mine[1] + 1u;
+    const uint32_t target = static_cast<uint32_t>(P) * n;
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - target) < 0) __nanosleep(64);
+    mine[1] = n;
   }
   __syncwarp();
 }
 
-// counts[E] of this rank's routing entries per global expert -> inbox of rank
-// d at row `rank`: inbox_d[rank * El + el] = counts[d * El + el].
-__global__ void k_ep_post_counts(const int32_t* __restrict__ counts, int32_t* const* __restrict__ peer_inbox, int P,
-                                 int El, int rank) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < P * El) {
-    const int d = e / El, el = e - d * El;
-    peer_inbox[d][rank * El + el] = counts[e];
-  }
-  __threadfence_system();
+__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
-// dest_base[d * El + el]: first row of (source = rank, expert el of d) in d's
-// receive buffer; off_local[0..El]: this rank's expert offsets over all sources.
-// One CTA, blockDim >= max(P * El, El + 1).
-__global__ void k_ep_plan(int32_t* const* __restrict__ peer_inbox, int P, int El, int rank,
-                          int32_t* __restrict__ dest_base, int32_t* __restrict__ off_local) {
-  extern __shared__ int32_t s_cnt[];  // [P dest][P src][El]
-  const int n = P * P * El;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int d = i / (P * El), rest = i - d * P * El;  // rest = src * El + el
-    s_cnt[i] = __ldcv(peer_inbox[d] + rest);
+// Count exchange + plan in ONE launch (one CTA; replaces post-counts, a full barrier and the
+// plan kernel). This rank's per-global-expert counts go to every rank's inbox[parity][rank],
+// followed by a system-scope release of ready[parity][rank] = layer + 1; the CTA then waits for
+// every source's tag in its OWN control block and plans from its own inbox:
+//   dest_base[d*El+el]: first row of (source = rank, expert el of d) in d's receive buffer
+//     (rows expert-major, source-rank-major within an expert, source order within a source);
+//   off_local[0..El]: this rank's expert offsets over all sources (off_local[El] = rows received).
+// Reusing inbox[parity] two layers later is safe: a rank posts layer n+2 only after its
+// exchange of layer n+1 saw every peer's tag n+2, which each peer posts after planning layer n.
+__global__ void __launch_bounds__(1024)
+    k_ep_exchange(const int32_t* __restrict__ counts, uint32_t* const* __restrict__ peer_ctl, int P, int El,
+                  int rank, int32_t* __restrict__ dest_base, int32_t* __restrict__ off_local) {
+  extern __shared__ int32_t s_cnt[];  // [P src][E]
+  __shared__ uint32_t s_layer;
+  const int E = P * El;
+  uint32_t* mine = peer_ctl[rank];
+  if (threadIdx.x == 0) s_layer = mine[2];
+  __syncthreads();
+  const uint32_t layer = s_layer;
+  const int parity = static_cast<int>(layer & 1u);
+  const size_t box = static_cast<size_t>(parity) * P * E + static_cast<size_t>(rank) * E;
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
+    const int d = i / E, e = i - d * E;
+    reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(peer_ctl[d]) + kCtlInbox)[box + e] = counts[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < P) st_release_sys(peer_ctl[threadIdx.x] + kCtlReadyWord + parity * kEpMaxRanks + rank, layer + 1u);
+  if (threadIdx.x < P) {
+    const uint32_t* tag = mine + kCtlReadyWord + parity * kEpMaxRanks + threadIdx.x;
+    while (ld_acquire_sys(tag) != layer + 1u) __nanosleep(32);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < P * El; i += blockDim.x) {
-    const int d = i / El, el = i - d * El;
-    const int32_t* c = s_cnt + d * P * El;  // c[src * El + e']
+  const int32_t* inbox = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(mine) + kCtlInbox) +
+                         static_cast<size_t>(parity) * P * E;
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) s_cnt[i] = __ldcv(inbox + i);  // L1 may hold layer n-2
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const int d = i / El;
     int base = 0;
-    for (int e2 = 0; e2 < el; ++e2)
-      for (int s = 0; s < P; ++s) base += c[s * El + e2];
-    for (int s = 0; s < rank; ++s) base += c[s * El + el];
+    for (int e2 = d * El; e2 < i; ++e2)
+      for (int s = 0; s < P; ++s) base += s_cnt[s * E + e2];
+    for (int s = 0; s < rank; ++s) base += s_cnt[s * E + i];
     dest_base[i] = base;
   }
-  for (int i = threadIdx.x; i <= El; i += blockDim.x) {  // El + 1 entries: El may reach blockDim.x
-    const int32_t* c = s_cnt + rank * P * El;
+  for (int i = threadIdx.x; i <= El; i += blockDim.x) {  // El + 1 entries
     int o = 0;
-    for (int e2 = 0; e2 < i; ++e2)
-      for (int s = 0; s < P; ++s) o += c[s * El + e2];
+    for (int e2 = rank * El; e2 < rank * El + i; ++e2)
+      for (int s = 0; s < P; ++s) o += s_cnt[s * E + e2];
     off_local[i] = o;
   }
+  if (threadIdx.x == 0) mine[2] = layer + 1u;
 }
 
 // Warp per routing entry i = t * topk + j: the token row goes straight into
@@ -117,17 +150,19 @@ __global__ void __launch_bounds__(256)
   __threadfence_system();
 }
 
-// CTA per token: y[t] = sum_j w[t,j] * y_out_{dest_rank}[dest_row] (fp32, fixed j order).
+// CTA per token: y[t] = sum_j w[t,j] * y_out_{dest_rank}[dest_row] (fp32, fixed j order), with
+// up to eight of the token's rows in flight per thread (L1 bypassed: the owners rewrite y_out
+// every layer).
 __global__ void __launch_bounds__(256)
     k_ep_combine(__nv_bfloat16* const* __restrict__ peer_y, const int32_t* __restrict__ dest_rank,
                  const int32_t* __restrict__ dest_row, const float* __restrict__ w, int T, int topk, int H,
                  __nv_bfloat16* __restrict__ y) {
   const int t = blockIdx.x;
-  __shared__ const __nv_bfloat16* s_row[32];
+  __shared__ const uint4* s_row[32];
   __shared__ float s_w[32];
   if (threadIdx.x < topk) {
     const int i = t * topk + threadIdx.x;
-    s_row[threadIdx.x] = peer_y[dest_rank[i]] + static_cast<size_t>(dest_row[i]) * H;
+    s_row[threadIdx.x] = reinterpret_cast<const uint4*>(peer_y[dest_rank[i]] + static_cast<size_t>(dest_row[i]) * H);
     s_w[threadIdx.x] = w[i];
   }
   __syncthreads();
@@ -135,15 +170,23 @@ __global__ void __launch_bounds__(256)
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-    for (int j = 0; j < topk; ++j) {
-      const uint4 d = __ldcv(reinterpret_cast<const uint4*>(s_row[j]) + v);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d);
-      const float wj = s_w[j];
+    for (int j0 = 0; j0 < topk; j0 += 8) {
+      uint4 d[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(h2[q]);
-        acc[2 * q] += wj * f.x;
-        acc[2 * q + 1] += wj * f.y;
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < topk) d[u] = __ldcg(s_row[j0 + u] + v);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < topk) {
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&d[u]);
+          const float wj = s_w[j0 + u];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(h2[q]);
+            acc[2 * q] += wj * f.x;
+            acc[2 * q + 1] += wj * f.y;
+          }
+        }
       }
     }
     uint4 o;

@@ -154,7 +154,7 @@ struct ExpertsCfg {
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kAuxBytes;
 };
 
-enum : int { kItemUp = 0, kItemDown = 1, kItemEnd = 2 };
+enum : int { kItemUp = 0, kItemDown = 1, kItemEnd = 2, kItemDnc = 3 };  // kItemDnc: k_decode only
 
 // SiLU(g) * u with one MUFU op: silu(g) = 0.5 g (1 + tanh(g / 2)); tanh.approx
 // (rel. err ~2^-11) is well below the bf16 rounding of the result.

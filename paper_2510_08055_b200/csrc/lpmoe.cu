@@ -589,6 +589,7 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
                   int32_t* tok_of, void* act, void* y_perm, uint32_t* sched, void* y, uint32_t* cmb, int wpol,
                   cudaStream_t st) {
   static const int warm = env_int("LPMOE_DECODE_W2_WARM", 1);
+  static const int dnc = env_int("LPMOE_DECODE_DNC", 1);
   int rc;
   if ((rc = get_encode())) return rc;
   const int S = T * topk;
@@ -598,6 +599,10 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
   if ((rc = make_tmap(&tm_w13h, w13, static_cast<uint64_t>(E) * 2 * I, H, 64))) return rc;
   if ((rc = make_tmap(&tm_w2, w2, static_cast<uint64_t>(E) * H, I, lp::kTileM))) return rc;
   if ((rc = make_tmap(&tm_act, act, S, I, lp::DecodeCfg::kN))) return rc;
+  // W2 boxes of 8/16/32/64 rows: the block-diagonal DN tiles of S <= 16 (R rows per hit expert)
+  CUtensorMap tm_w2r[4];
+  for (int i = 0; i < 4; ++i)
+    if ((rc = make_tmap(&tm_w2r[i], w2, static_cast<uint64_t>(E) * H, I, 8u << i))) return rc;
   constexpr int smem = lp::DecodeCfg::kSmemBytes;
   static const int forced_cs = env_int("LPMOE_DECODE_CS", 0);
   const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 4 ? 4 : 2);
@@ -606,7 +611,7 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
   const lp::DecodeParams p{T, H, I, E, topk, renorm, static_cast<const __nv_bfloat16*>(x),
                            static_cast<const uint8_t*>(w2), ids, w, counts, offsets, slot_of, tok_of,
                            static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0};
+                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0, dnc != 0 ? 1 : 0};
   // clusters of 4 that are co-resident (GPC boundaries can leave SMs that no 4-CTA cluster fits):
   // a second wave would repeat the routing prologue after the first wave's stream
   static std::mutex mu;
@@ -639,7 +644,7 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
     grid = g;
   }
   LP_CUDA(launch_pdl_cluster(kern, grid, lp::DecodeCfg::kThreads, smem, st, cs, tm_wr, tm_x, tm_w13h, tm_w2, tm_act,
-                             p));
+                             tm_w2r[0], tm_w2r[1], tm_w2r[2], tm_w2r[3], p));
   return LP_OK;
 }
 
@@ -1073,33 +1078,32 @@ int lp_ipc_close(void* dptr) {
   return ok();
 }
 
-int lp_ep_barrier(uint32_t* const* peer_flag, int P, int rank, uint32_t target, void* stream) {
-  if (P < 1 || rank < 0 || rank >= P || !peer_flag) return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
+size_t lp_ep_ctl_bytes(int P, int E) {
+  if (P < 1 || P > lp::kEpMaxRanks || E < P || E % P) return 0;
+  return static_cast<size_t>(lp::kCtlInbox) + 2u * static_cast<size_t>(P) * E * sizeof(int32_t);
+}
+
+int lp_ep_barrier(uint32_t* const* peer_ctl, int P, int rank, void* stream) {
+  if (P < 1 || P > lp::kEpMaxRanks || rank < 0 || rank >= P || !peer_ctl)
+    return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
   count_launch();
-  lp::k_ep_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(peer_flag, P, rank, target);
+  lp::k_ep_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(peer_ctl, P, rank);
   LP_CHECK_LAUNCH("k_ep_barrier");
   return ok();
 }
 
-int lp_ep_post_counts(const int32_t* counts, int32_t* const* peer_inbox, int P, int El, int rank, void* stream) {
-  if (P < 1 || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !counts || !peer_inbox)
-    return fail(LP_EINVAL, "lp_ep_post_counts: bad arguments P=%d El=%d rank=%d", P, El, rank);
-  count_launch();
-  lp::k_ep_post_counts<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(counts, peer_inbox, P, El, rank);
-  LP_CHECK_LAUNCH("k_ep_post_counts");
-  return ok();
-}
-
-int lp_ep_plan(int32_t* const* peer_inbox, int P, int El, int rank, int32_t* dest_base, int32_t* off_local,
-               void* stream) {
-  if (P < 1 || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !peer_inbox || !dest_base ||
-      !off_local)
-    return fail(LP_EINVAL, "lp_ep_plan: bad arguments P=%d El=%d rank=%d", P, El, rank);
+int lp_ep_exchange(const int32_t* counts, uint32_t* const* peer_ctl, int P, int El, int rank, int32_t* dest_base,
+                   int32_t* off_local, void* stream) {
+  if (P < 1 || P > lp::kEpMaxRanks || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !counts ||
+      !peer_ctl || !dest_base || !off_local)
+    return fail(LP_EINVAL, "lp_ep_exchange: bad arguments P=%d El=%d rank=%d", P, El, rank);
   const size_t sm = static_cast<size_t>(P) * P * El * sizeof(int32_t);
-  if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_plan: P*P*El too large");
+  if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_exchange: P*P*El too large");
   count_launch();
-  lp::k_ep_plan<<<1, 256, sm, static_cast<cudaStream_t>(stream)>>>(peer_inbox, P, El, rank, dest_base, off_local);
-  LP_CHECK_LAUNCH("k_ep_plan");
+  const int threads = P * El + 1 > 256 ? 512 : 256;  // >= El + 1 not required (strided), >= P is
+  lp::k_ep_exchange<<<1, threads, sm, static_cast<cudaStream_t>(stream)>>>(counts, peer_ctl, P, El, rank,
+                                                                          dest_base, off_local);
+  LP_CHECK_LAUNCH("k_ep_exchange");
   return ok();
 }
 

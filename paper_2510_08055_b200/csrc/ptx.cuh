@@ -307,8 +307,10 @@ __device__ __forceinline__ void lp_trace_max(int slot) {
   atomicMax(&g_lp_trace[slot], t);
 }
 // per-CTA work-item timeline of the decode-size expert kernel: [cta][item][field]
-// fields: 0 item id, 1 claimed, 2 dependency met (DN) / claimed (UP), 3 last TMA issued, 4 epilogue done
-constexpr int kTraceCtas = 160, kTraceItems = 8, kTraceFields = 5;
+// fields: 0 item id, 1 claimed, 2 dependency met (DN) / claimed (UP), 3 last TMA issued, 4 epilogue done,
+// 5 first MMA issued, 6 last MMA issued (commit), 7 accumulator received by the epilogue,
+// 8 k-block kbl-2 ready (A and B landed), 9 k-block kbl-1 ready
+constexpr int kTraceCtas = 160, kTraceItems = 8, kTraceFields = 10;
 __device__ unsigned long long g_lp_items[kTraceCtas * kTraceItems * kTraceFields];
 __device__ __forceinline__ unsigned long long lp_now() {
   unsigned long long t;

@@ -201,19 +201,24 @@ class EPMoE:
 class PeerRegion:
     """One rank's symmetric EP buffers, exported over CUDA IPC and mapped by every rank.
 
-    Layout (256-byte aligned): [barrier counter | per-source expert counts
-    (P x El int32) | recv_x [cap, H] bf16 | y_out [cap, H] bf16], allocated with
-    plain cudaMalloc (lp_ipc_alloc). `peer_*` are device arrays of the P ranks'
-    addresses of each part. The layers of one stack run in sequence and share
-    one region (and its barrier epoch). `group` is used once, to swap handles.
+    Layout (256-byte aligned): [control block: barrier counter, barrier / layer
+    sequence numbers, ready tags, double-buffered count inbox [2][P][E] int32
+    (lp_ep_ctl_bytes) | recv_x [cap, H] bf16 | y_out [cap, H] bf16], allocated
+    with plain cudaMalloc (lp_ipc_alloc, zero-filled). `peer_*` are device arrays
+    of the P ranks' addresses of each part. The layers of one stack run in
+    sequence and share one region; its sequence numbers live on the device, so
+    layers are CUDA-graph capturable. `group` is used to swap handles and to
+    fence `close()`.
     """
 
     def __init__(self, device: torch.device, rank: int, world: int, cap: int, hidden: int, el: int, group=None):
         self.device, self.rank, self.world, self.cap, self.hidden, self.el = device, rank, world, cap, hidden, el
+        self.group = group
         self.lib = _native.load()
         align = lambda n: (n + 255) // 256 * 256  # noqa: E731
-        off_flag, off_inbox = 0, 256
-        off_recv = align(off_inbox + 4 * world * el)
+        ctl = int(self.lib.lp_ep_ctl_bytes(world, world * el))
+        require(ctl > 0, f"PeerRegion: unsupported EP world size {world} (max 32) for {world * el} experts")
+        off_recv = align(ctl)
         off_y = align(off_recv + 2 * cap * hidden)
         total = align(off_y + 2 * cap * hidden)
         base = ctypes.c_void_p(0)
@@ -235,11 +240,10 @@ class PeerRegion:
             self._opened.append(int(p.value))
             bases.append(int(p.value) + o)
         arr = lambda o: torch.tensor([b + o for b in bases], dtype=torch.int64, device=device)  # noqa: E731
-        self.peer_flag, self.peer_inbox = arr(off_flag), arr(off_inbox)
+        self.peer_ctl = arr(0)
         self.peer_recv, self.peer_y = arr(off_recv), arr(off_y)
         self.recv_x_ptr = self.base + off_recv  # [cap, H] bf16
         self.y_out_ptr = self.base + off_y      # [cap, H] bf16
-        self.epoch = 0
         self._act: torch.Tensor | None = None
         self.dest_base = torch.empty((world * el,), dtype=torch.int32, device=device)
         self.off_local = torch.empty((el + 1,), dtype=torch.int32, device=device)
@@ -253,16 +257,25 @@ class PeerRegion:
 
     def barrier(self, stream) -> None:
         """Device-side barrier over the P ranks, ordered on `stream`."""
-        self.epoch += 1
-        _native.check(self.lib.lp_ep_barrier(self.peer_flag.data_ptr(), self.world, self.rank,
-                                             self.world * self.epoch, stream), "lp_ep_barrier")
+        _native.check(self.lib.lp_ep_barrier(self.peer_ctl.data_ptr(), self.world, self.rank, stream),
+                      "lp_ep_barrier")
+
+    def exchange(self, counts: torch.Tensor, stream) -> None:
+        """Post this rank's per-global-expert counts to every rank, wait for every source's, plan
+        dest_base / off_local (one launch)."""
+        _native.check(self.lib.lp_ep_exchange(counts.data_ptr(), self.peer_ctl.data_ptr(), self.world, self.el,
+                                              self.rank, self.dest_base.data_ptr(), self.off_local.data_ptr(),
+                                              stream), "lp_ep_exchange")
 
     def close(self) -> None:
+        """Collective: every rank must call it (peers may still read this region until all have synced)."""
+        if self.base:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
         for p in self._opened:
             self.lib.lp_ipc_close(p)
         self._opened = []
         if self.base:
-            torch.cuda.synchronize(self.device)
             self.lib.lp_ipc_free(self.base)
             self.base = 0
 
@@ -299,13 +312,27 @@ class PeerEP:
             _check_tensor(name, t, shp, torch.bfloat16)
         self.wr, self.w13, self.w2 = wr, w13_local, w2_local
         self.lib = _native.load()
-        self.ops = GpuOps(self.device)
         cap = max_tokens * k * world  # worst case: every rank's entries land on this rank
         if region is None:
             region = PeerRegion(self.device, rank, world, cap, H, self.el, group)
         require(region.world == world and region.rank == rank and region.cap >= cap and region.hidden == H
                 and region.el == self.el, "region: incompatible PeerRegion for this layer")
         self.region = region
+        # per-layer buffers sized once for max_tokens (no allocation on the layer path); the stats a
+        # call returns alias them and stay valid until this layer's next call
+        dev, S = self.device, max_tokens * k
+        self._ids = torch.empty((max_tokens, k), dtype=torch.int32, device=dev)
+        self._w = torch.empty((max_tokens, k), dtype=torch.float32, device=dev)
+        self._counts = torch.zeros((E,), dtype=torch.int32, device=dev)
+        self._offsets = torch.zeros((E + 1,), dtype=torch.int32, device=dev)
+        self._slot_of = torch.empty((S,), dtype=torch.int32, device=dev)
+        self._tok_of = torch.empty((S,), dtype=torch.int32, device=dev)
+        self._dest_rank = torch.empty((S,), dtype=torch.int32, device=dev)
+        self._dest_row = torch.empty((S,), dtype=torch.int32, device=dev)
+        self._recv_rows = torch.zeros((1,), dtype=torch.int32, device=dev)
+        need = max(int(self.lib.lp_moe_workspace_bytes(max_tokens, H, 128, E, k)),   # route + permute
+                   int(self.lib.lp_moe_workspace_bytes(1, H, shape.ffn, self.el, 1)))  # expert tile plan
+        self._ws = torch.zeros(need, dtype=torch.uint8, device=dev)
 
     @classmethod
     def from_full(cls, shape: MoEShape, wr, w13, w2, rank: int, world: int, max_tokens: int, group=None,
@@ -316,56 +343,51 @@ class PeerEP:
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, prof=None) -> tuple[torch.Tensor, EPStats]:
         """prof: optional list of 5 CUDA events recorded at the stage boundaries (start | route +
-        permute | counts + dispatch | experts | combine) for bench.py's per-rank stage split."""
+        permute | exchange + dispatch | experts | combine) for bench.py's per-rank stage split.
+        Every rank must call every layer (a rank with T = 0 still takes part in the exchange)."""
         s, P, el, lib, rg = self.shape, self.world, self.el, self.lib, self.region
         mark = (lambda i: prof[i].record()) if prof is not None else (lambda i: None)
         require(x.dim() == 2 and x.shape[1] == s.hidden, f"x must be [T, {s.hidden}], got {tuple(x.shape)}")
-        T, H, k = x.shape[0], s.hidden, s.top_k
+        T, H, k, E = x.shape[0], s.hidden, s.top_k, s.num_experts
         require(T <= self.max_tokens, f"T={T} exceeds max_tokens={self.max_tokens}")
+        _check_tensor("x", x, (T, H), torch.bfloat16)
         st = _stream_ptr(self.device)
+        ws = self._ws
+        # (pointers from the full buffers: an empty view's data_ptr() is 0, which the ABI rejects)
+        ids, w, counts = self._ids[:T], self._w[:T], self._counts
         mark(0)
-        ids, w = self.ops.route(x, self.wr, k, s.norm_topk_prob)
-        counts = torch.zeros((s.num_experts,), dtype=torch.int32, device=self.device)
-        offsets = torch.zeros((s.num_experts + 1,), dtype=torch.int32, device=self.device)
-        S = T * k
-        slot_of = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
-        tok_of = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
-        if T:  # index-only permutation: slots within each (global) expert, no x_perm
-            ws = self.ops._workspace(T, H, 128, s.num_experts, k)
-            _native.check(lib.lp_moe_permute(ids.data_ptr(), x.data_ptr(), T, H, s.num_experts, k, counts.data_ptr(),
-                                             offsets.data_ptr(), slot_of.data_ptr(), tok_of.data_ptr(), None,
-                                             ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
+        if T:  # route, then the index-only permutation: slots within each (global) expert, no x_perm
+            _native.check(lib.lp_moe_route(x.data_ptr(), self.wr.data_ptr(), T, H, E, k, int(s.norm_topk_prob),
+                                           self._ids.data_ptr(), self._w.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                          "lp_moe_route")
+        _native.check(lib.lp_moe_permute(self._ids.data_ptr(), x.data_ptr(), T, H, E, k, counts.data_ptr(),
+                                         self._offsets.data_ptr(), self._slot_of.data_ptr(), self._tok_of.data_ptr(),
+                                         None, ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
         mark(1)
-        _native.check(lib.lp_ep_post_counts(counts.data_ptr(), rg.peer_inbox.data_ptr(), P, el, self.rank, st),
-                      "lp_ep_post_counts")
-        rg.barrier(st)
-        _native.check(lib.lp_ep_plan(rg.peer_inbox.data_ptr(), P, el, self.rank, rg.dest_base.data_ptr(),
-                                     rg.off_local.data_ptr(), st), "lp_ep_plan")
-        dest_rank = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
-        dest_row = torch.empty((max(S, 1),), dtype=torch.int32, device=self.device)
-        _native.check(lib.lp_ep_dispatch(x.data_ptr(), ids.data_ptr(), slot_of.data_ptr(), offsets.data_ptr(),
-                                         rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(), T, H, k, el,
-                                         dest_rank.data_ptr(), dest_row.data_ptr(), st), "lp_ep_dispatch")
+        rg.exchange(counts, st)  # counts to every rank + wait for every source + plan (one launch)
+        _native.check(lib.lp_ep_dispatch(x.data_ptr(), self._ids.data_ptr(), self._slot_of.data_ptr(),
+                                         self._offsets.data_ptr(), rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(),
+                                         T, H, k, el, self._dest_rank.data_ptr(), self._dest_row.data_ptr(), st),
+                      "lp_ep_dispatch")
         rg.barrier(st)
         mark(2)
         # rows received stay on the device (off_local[El]): capacity-sized launch, tile width from the
         # expected T*k rows; no host sync, so the whole layer is stream-ordered and graph-capturable
         act = rg.act(s.ffn)
-        ws = self.ops._workspace(1, H, s.ffn, el, 1)  # header + tile plan only (rows live in the region)
         _native.check(lib.lp_moe_experts_rows(rg.recv_x_ptr, rg.off_local.data_ptr(), rg.cap, max(T, 1) * k,
                                               self.w13.data_ptr(), self.w2.data_ptr(), H, s.ffn, el,
                                               act.data_ptr(), rg.y_out_ptr, ws.data_ptr(), ws.numel(), st),
                       "lp_moe_experts_rows")
+        self._recv_rows.copy_(rg.off_local[el:el + 1])  # the region's off_local is rewritten by the next layer
         rg.barrier(st)
         mark(3)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
-        _native.check(lib.lp_ep_combine(rg.peer_y.data_ptr(), dest_rank.data_ptr(), dest_row.data_ptr(),
-                                        w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
-        rg.barrier(st)
+        _native.check(lib.lp_ep_combine(rg.peer_y.data_ptr(), self._dest_rank.data_ptr(), self._dest_row.data_ptr(),
+                                        self._w.data_ptr(), T, H, k, y.data_ptr(), st), "lp_ep_combine")
+        # no end-of-layer barrier: see ep_p2p.cuh (the next exchange / dispatch barrier orders reuse)
         mark(4)
         self.last_ids, self.last_weights = ids, w
-        # recv_rows: a stream-ordered copy (the region's off_local is rewritten by the next layer)
-        return y, EPStats(counts, rg.off_local[el].clone(), counts.view(P, el).sum(1), [], s)
+        return y, EPStats(counts, self._recv_rows[0], counts.view(P, el).sum(1), [], s)
 
     __call__ = forward
 

@@ -28,6 +28,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import torch
+import torch.distributed as dist
 
 from .moe import GpuMoE, Workspace, add_rmsnorm
 from .synthetic import router_weight
@@ -123,21 +124,22 @@ class MoEModel:
         self.layers: list[GpuMoE] = []
         self.workspace = Workspace(self.device)  # one scratch for the whole stack (layers run in order)
         for i in range(num_layers):
-            g = torch.Generator(device=self.device).manual_seed(seed * 1000 + i)
-            E, H, I = shape.num_experts, shape.hidden, shape.ffn
-            w13 = (torch.randn((E, 2 * I, H), generator=g, device=self.device) * std).to(torch.bfloat16)
-            w2 = (torch.randn((E, H, I), generator=g, device=self.device) * std).to(torch.bfloat16)
-            wr = router_weight(E, H, seed * 1000 + i).to(self.device)
+            wr, w13, w2 = layer_weights(shape, self.device, seed, i, std)
             self.layers.append(GpuMoE(shape, wr, w13, w2, workspace=self.workspace))
         # decode-size segments (T <= graph_tokens) replay per-layer CUDA graphs
         self.graphs = _DecodeGraphs(self, graph_tokens) if graph_tokens > 0 else None
 
-    def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor) -> torch.Tensor:
+    def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor, events=None) -> torch.Tensor:
         """h <- h + MoE_l(RMSNorm(h)) for l in [l0, l1) (Qwen3's pre-MoE norm keeps the
-        residual stream bounded); per-expert counts of layer l are added into counts[l]."""
+        residual stream bounded); per-expert counts of layer l are added into counts[l].
+        events: a list that receives the (start, end) CUDA events around the MoE work."""
         T = x.shape[0]
+        e0, e1 = _timed(events)
+        e0.record()
         if self.graphs is not None and 0 < T <= self.graphs.max_tokens:
-            return self.graphs.run_segment(x, l0, l1, counts)
+            x = self.graphs.run_segment(x, l0, l1, counts)
+            e1.record()
+            return x
         xn = torch.empty_like(x)
         y = torch.empty_like(x)
         c = torch.empty((l1 - l0, self.shape.num_experts), dtype=torch.int32, device=self.device)
@@ -148,8 +150,131 @@ class MoEModel:
             delta = y
         if delta is not None and T:
             add_rmsnorm(x, delta, xn)
+        e1.record()
         counts[l0:l1] += c
         return x
+
+    # single device: nothing to reduce across ranks
+    def reduce_max(self, v: float) -> float:
+        return v
+
+    def reduce_counts(self, counts: torch.Tensor) -> torch.Tensor:
+        return counts
+
+
+def layer_weights(shape: MoEShape, device: torch.device, seed: int, i: int, std: float = 0.02):
+    """Random-init weights of layer i (router on the dyadic grid, experts N(0, std^2) in bf16): the
+    single-GPU and expert-parallel stacks build identical layers from the same seed."""
+    g = torch.Generator(device=device).manual_seed(seed * 1000 + i)
+    E, H, I = shape.num_experts, shape.hidden, shape.ffn
+    w13 = (torch.randn((E, 2 * I, H), generator=g, device=device) * std).to(torch.bfloat16)
+    w2 = (torch.randn((E, H, I), generator=g, device=device) * std).to(torch.bfloat16)
+    wr = router_weight(E, H, seed * 1000 + i).to(device)
+    return wr, w13, w2
+
+
+def _timed(events):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if events is not None:
+        events.append((e0, e1))
+    return e0, e1
+
+
+class EPMoEModel:
+    """`num_layers` expert-parallel MoE layers (BASELINE config 5): rank r of P holds
+    experts [r*E/P, (r+1)*E/P) of every layer (ep.PeerEP: fused dispatch / combine over peer
+    memory, one PeerRegion shared by the stack). The MoE is token-data-parallel: every rank keeps
+    the full hidden state (replicated, as attention/dense would produce it), runs the layers on
+    its contiguous share of each segment's rows, and the processed rows are all-gathered back
+    after the segment (outside the timed MoE region: it stands for the attention's own exchange).
+    Per token the math is the single-GPU layer's, so hidden states are bit-identical to MoEModel
+    built from the same seed (tests/test_gpu_ep_executor.py). Every rank must run every segment.
+    max_tokens: the largest segment (all ranks' rows) the stack will see."""
+
+    def __init__(self, shape: MoEShape, num_layers: int, rank: int, world: int, max_tokens: int,
+                 device="cuda", seed: int = 0, std: float = 0.02, group=None):
+        from .ep import PeerEP
+
+        self.shape, self.num_layers, self.rank, self.world, self.group = shape, num_layers, rank, world, group
+        self.device = torch.device(device)
+        self.max_local = (max_tokens + world - 1) // world
+        el = shape.num_experts // world
+        sl = slice(rank * el, (rank + 1) * el)
+        self.layers: list = []
+        region = None
+        for i in range(num_layers):
+            wr, w13, w2 = layer_weights(shape, self.device, seed, i, std)
+            ep = PeerEP(shape, wr, w13[sl].contiguous(), w2[sl].contiguous(), rank, world, self.max_local,
+                        group=group, region=region)
+            del w13, w2
+            region = ep.region
+            self.layers.append(ep)
+        self.region = region
+        self.graphs = None
+        self._gloo = dist.get_backend(group) != "nccl"
+
+    def _rows(self, T: int) -> tuple[int, int]:
+        return T * self.rank // self.world, T * (self.rank + 1) // self.world
+
+    def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor, events=None) -> torch.Tensor:
+        T, H = x.shape
+        lo, hi = self._rows(T)
+        xl = x[lo:hi]
+        xn = torch.empty_like(xl)
+        y = torch.empty_like(xl)
+        e0, e1 = _timed(events)
+        e0.record()
+        delta = None
+        for layer in range(l0, l1):
+            add_rmsnorm(xl, delta, xn)
+            _, st = self.layers[layer](xn, out=y)
+            counts[layer] += st.counts
+            delta = y
+        if delta is not None and hi > lo:
+            add_rmsnorm(xl, delta, xn)
+        e1.record()
+        return self._gather(x, xl)
+
+    def _gather(self, x: torch.Tensor, xl: torch.Tensor) -> torch.Tensor:
+        """Every rank's processed rows back into the replicated x (uneven shares padded)."""
+        T, H = x.shape
+        P = self.world
+        n = (T + P - 1) // P
+        pad = torch.zeros((n, H), dtype=x.dtype, device=x.device)
+        pad[: xl.shape[0]].copy_(xl)
+        if self._gloo:  # protocol tests: ranks share one GPU, collectives staged through the host
+            parts = [torch.empty((n, H), dtype=x.dtype) for _ in range(P)]
+            dist.all_gather(parts, pad.cpu(), group=self.group)
+            full = torch.cat(parts).to(x.device)
+        else:
+            full = torch.empty((P * n, H), dtype=x.dtype, device=x.device)
+            dist.all_gather_into_tensor(full, pad, group=self.group)
+        for r in range(P):
+            a, b = T * r // P, T * (r + 1) // P
+            if r != self.rank and b > a:
+                x[a:b].copy_(full[r * n: r * n + (b - a)])
+        return x
+
+    def _reduce(self, t: torch.Tensor, op) -> torch.Tensor:
+        if self._gloo:
+            c = t.cpu()
+            dist.all_reduce(c, op=op, group=self.group)
+            return c.to(t.device)
+        dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def reduce_max(self, v: float) -> float:
+        """MoE device time of an iteration: the slowest rank's (the layers barrier every rank)."""
+        return float(self._reduce(torch.tensor([v], dtype=torch.float64, device=self.device), dist.ReduceOp.MAX)[0])
+
+    def reduce_counts(self, counts: torch.Tensor) -> torch.Tensor:
+        """Per-layer expert counts of all ranks' tokens (experts hit = nnz of the sum)."""
+        return self._reduce(counts.clone(), dist.ReduceOp.SUM)
+
+    def close(self) -> None:
+        if self.region is not None:
+            self.region.close()
+            self.region = None
 
 
 @dataclass
@@ -217,7 +342,6 @@ class LayeredExecutor:
         for a in plan.prefill_assignments:
             for layer in range(a.layer_start, a.layer_end):
                 routed[layer] += a.num_tokens
-        stream = torch.cuda.current_stream(self.dev)
         events = []
         dec = torch.stack(dec_rows) if D else torch.empty((0, self.H), dtype=torch.bfloat16, device=self.dev)
         for l0, l1 in zip(cuts, cuts[1:]):
@@ -226,12 +350,9 @@ class LayeredExecutor:
             if sum(p.shape[0] for p in parts) == 0:
                 continue
             x = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
-            # only the layer calls are timed (not the embedding, the concatenation or the copy-back)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            x = self.stack.run_segment(x, l0, l1, counts)
-            e1.record(stream)
-            events.append((e0, e1))
+            # only the MoE work is timed (not the embedding, the concatenation, the copy-back or an
+            # expert-parallel stack's row gather): the stack records the events
+            x = self.stack.run_segment(x, l0, l1, counts, events)
             dec = x[:D]
             off = D
             for a in act:
@@ -241,8 +362,8 @@ class LayeredExecutor:
         for rid, row in zip(plan.decode_ids, dec):
             self.decode_row[rid] = row
         torch.cuda.synchronize(self.dev)
-        moe_s = sum(a.elapsed_time(b) for a, b in events) * 1e-3
-        nnz = (counts > 0).sum(dim=1).cpu().tolist()
+        moe_s = self.stack.reduce_max(sum(a.elapsed_time(b) for a, b in events) * 1e-3)
+        nnz = (self.stack.reduce_counts(counts) > 0).sum(dim=1).cpu().tolist()
         self.iter_log.append({"moe_s": moe_s, "routed": routed, "experts_hit": nnz, "decode": D,
                               "prefill_tokens": plan.prefill_tokens})
         # drop finished requests' state (the engine retires them after this call)

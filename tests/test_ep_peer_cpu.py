@@ -41,24 +41,30 @@ def _worker(rank, world, port, tokens, skew, bufs, q):
         P, E, k = world, SHAPE.num_experts, SHAPE.top_k
         El = E // P
         wr, w13, w2 = _weights(skew)
-        x = router_tokens(tokens[rank], SHAPE.hidden, 40 + rank).float().numpy()
-        ids, w, _ = mo.route(x, wr, k, SHAPE.norm_topk_prob)
-        counts, offsets, slot_of, _ = mo.permute(ids, E)
-        ep_peer.post_counts(counts, [b.numpy() for b in inbox], P, El, rank)
-        dist.barrier()
-        dest_base, off_local = ep_peer.plan([b.numpy() for b in inbox], P, El, rank)
-        dest_rank, dest_row = ep_peer.dispatch(x, ids, slot_of, offsets, dest_base, [b.numpy() for b in recv], El)
-        dist.barrier()
-        R = int(off_local[El])
-        _, yl = mo.experts(recv[rank].numpy()[:R], off_local, w13[rank * El:(rank + 1) * El],
-                           w2[rank * El:(rank + 1) * El])
-        y_out[rank].numpy()[:R] = yl
-        dist.barrier()
-        y = ep_peer.combine([b.numpy() for b in y_out], dest_rank, dest_row, w)
-        ref = mo.moe_forward(x, wr, w13, w2, k, SHAPE.norm_topk_prob)["y"]
-        ok = np.allclose(y, ref, rtol=1e-5, atol=1e-6) and R == int(np.asarray(inbox[rank]).sum())
-        dist.barrier()
-        q.put((rank, bool(ok), float(np.abs(y - ref).max()) if y.size else 0.0))
+        ok, err = True, 0.0
+        for layer in range(3):  # the inbox is double-buffered by layer parity
+            x = router_tokens(tokens[rank], SHAPE.hidden, 40 + 10 * layer + rank).float().numpy()
+            ids, w, _ = mo.route(x, wr, k, SHAPE.norm_topk_prob)
+            counts, offsets, slot_of, _ = mo.permute(ids, E)
+            ep_peer.post_counts(counts, [b.numpy() for b in inbox], rank, layer)
+            dist.barrier()  # the GPU waits for every source's ready tag instead
+            dest_base, off_local = ep_peer.plan(inbox[rank].numpy(), P, El, rank, layer)
+            dest_rank, dest_row = ep_peer.dispatch(x, ids, slot_of, offsets, dest_base,
+                                                   [b.numpy() for b in recv], El)
+            dist.barrier()
+            R = int(off_local[El])
+            _, yl = mo.experts(recv[rank].numpy()[:R], off_local, w13[rank * El:(rank + 1) * El],
+                               w2[rank * El:(rank + 1) * El])
+            y_out[rank].numpy()[:R] = yl
+            dist.barrier()
+            y = ep_peer.combine([b.numpy() for b in y_out], dest_rank, dest_row, w)
+            ref = mo.moe_forward(x, wr, w13, w2, k, SHAPE.norm_topk_prob)["y"]
+            rows = int(np.asarray(inbox[rank])[layer & 1].reshape(P, P, El)[:, rank, :].sum())
+            ok &= bool(np.allclose(y, ref, rtol=1e-5, atol=1e-6)) and R == rows
+            err = max(err, float(np.abs(y - ref).max()) if y.size else 0.0)
+            # no end-of-layer barrier on the GPU; here one keeps y_out/recv reuse of the CPU test simple
+            dist.barrier()
+        q.put((rank, bool(ok), err))
     finally:
         dist.destroy_process_group()
 
@@ -70,7 +76,7 @@ def _run(tokens, skew=False, world=2):
     s.close()
     cap = sum(tokens) * SHAPE.top_k
     El = SHAPE.num_experts // world
-    bufs = ([torch.zeros(world * El, dtype=torch.int64).share_memory_() for _ in range(world)],
+    bufs = ([torch.zeros((2, world, world * El), dtype=torch.int64).share_memory_() for _ in range(world)],
             [torch.zeros((max(cap, 1), SHAPE.hidden), dtype=torch.float32).share_memory_() for _ in range(world)],
             [torch.zeros((max(cap, 1), SHAPE.hidden), dtype=torch.float32).share_memory_() for _ in range(world)])
     ctx = mp.get_context("spawn")

@@ -400,7 +400,7 @@ def test_decode_kernel_bit_identical_to_staged_path(cuda):
         "d = torch.device('cuda', 0); out = {}; g = torch.Generator().manual_seed(5)",
         "for si, s in enumerate([QWEN3_30B_A3B, MoEShape(256, 128, 16, 2, False)]):",
         "    layer = make(s, 81, d)[3]",
-        "    for T in (1, 4, 8):",
+        "    for T in (1, 2, 4, 8):",
         "        for kind in ('dy', 'gs'):",
         "            x = router_tokens(T, s.hidden, 90 + T) if kind == 'dy' else "
         "torch.randn((T, s.hidden), generator=g).to(torch.bfloat16)",

@@ -14,6 +14,13 @@ coverage).
   python tools/serving_bench.py --config c3        # 8192-token prompt + 32 concurrent decodes
   python tools/serving_bench.py --config c4        # chunk-size / layer-group sweep on an 8192-token prompt
   python tools/serving_bench.py --config c5 [--requests 100]   # configs/qwen_arxiv_layered.toml workload
+  python tools/serving_bench.py --config c5 --gpus 8           # expert-parallel stack, one rank per GPU
+
+With --gpus N > 1 the N ranks (started with torchrun unless WORLD_SIZE is set) each hold E/N
+experts of every layer (executor.EPMoEModel: ep.PeerEP over peer memory) and run the same
+reference-planned iterations on their share of each segment's rows; the MoE time charged is the
+slowest rank's. Rank 0 prints. LPMOE_BENCH_SHARED_GPU=1 puts every rank on cuda:0 over gloo
+(protocol check only: the ranks time-slice one GPU).
 
 Prints one JSON object per run on stdout.
 """
@@ -33,6 +40,7 @@ from paper_2510_08055_b200.types import QWEN3_30B_A3B, QWEN3_30B_A3B_MODEL  # no
 
 ms = refdrive.import_moesim()
 MODEL = refdrive.reference_model(QWEN3_30B_A3B_MODEL)
+EMIT = True  # rank 0 prints
 SLO = ms.types.SloSpec(ttft_slo_s=10.0, tbt_slo_s=0.125)  # configs/qwen_arxiv_layered.toml [slo]
 
 
@@ -72,9 +80,14 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
     m = ms.metrics.summarize(mres, SLO).to_dict()
     out["reference_model_h100"] = {k: m[k] for k in ("ttft_mean_s", "tbt_mean_s", "total_expert_load_bytes",
                                                      "num_iterations")}
-    if emit:
+    out["gpus"] = getattr(stack, "world", 1)
+    if emit and EMIT:
         print(json.dumps(out), flush=True)
     return out
+
+
+def _shared_gpu() -> bool:
+    return os.environ.get("LPMOE_BENCH_SHARED_GPU", "0") == "1"
 
 
 def main():
@@ -86,16 +99,48 @@ def main():
                     help="replay per-layer CUDA graphs for decode segments up to this many rows (0: eager)")
     ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (moesim workload.export_trace) "
                                                  "instead of the config's generated workload")
+    ap.add_argument("--gpus", type=int, default=1, help="expert-parallel ranks (one per GPU)")
+    ap.add_argument("--max-tokens", type=int, default=40960,
+                    help="--gpus > 1: the largest segment (rows of one layer call, all ranks) to size EP buffers")
     a = ap.parse_args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        import subprocess
 
-    from paper_2510_08055_b200.executor import MoEModel
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        sys.exit(subprocess.call([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+                                  os.path.abspath(__file__), *sys.argv[1:]]))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"serving_bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
+
+    import torch
+
+    from paper_2510_08055_b200.executor import EPMoEModel, MoEModel
 
     t0 = time.time()
-    stack = MoEModel(QWEN3_30B_A3B, MODEL.num_layers, device="cuda", seed=11, graph_tokens=a.graph_tokens)
+    if world > 1:
+        import torch.distributed as dist
+
+        dev = torch.device("cuda", 0 if _shared_gpu() else int(os.environ.get("LOCAL_RANK", 0)))
+        torch.cuda.set_device(dev)
+        dist.init_process_group("gloo" if _shared_gpu() else "nccl")
+        stack = EPMoEModel(QWEN3_30B_A3B, MODEL.num_layers, rank, world, a.max_tokens, device=dev, seed=11)
+        a.graph_tokens = 0  # (per-layer graphs are a single-GPU path)
+    else:
+        stack = MoEModel(QWEN3_30B_A3B, MODEL.num_layers, device="cuda", seed=11, graph_tokens=a.graph_tokens)
     if stack.graphs is not None:  # decode-only layer steps replay CUDA graphs (captured up front)
         stack.graphs.capture(range(1, a.graph_tokens + 1))
-    print(json.dumps({"setup": "48 resident layers", "seconds": time.time() - t0,
-                      "decode_graph_tokens": a.graph_tokens}), flush=True)
+    global EMIT
+    EMIT = rank == 0
+    if EMIT:
+        print(json.dumps({"setup": "48 resident layers", "seconds": time.time() - t0, "gpus": world,
+                          "experts_per_gpu": QWEN3_30B_A3B.num_experts // world,
+                          "decode_graph_tokens": a.graph_tokens}), flush=True)
     g = a.graph_tokens
     R = ms.types.Request
     L = a.prompt
@@ -124,7 +169,10 @@ def main():
             reqs = ms.workload.generate_requests(cfg.workload)[: a.requests]
         run_one(stack, "warmup", "layered", 512, 512, reqs[:10], emit=False)
         for policy in ("layered", "chunked"):
-            run_one(stack, f"c5_{policy}", policy, 512, 512, reqs, graphs=g)
+            run_one(stack, f"c5_{policy}" + (f"_ep{world}" if world > 1 else ""), policy, 512, 512, reqs, graphs=g)
+    if world > 1:
+        stack.close()
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -35,8 +35,9 @@ NAMES = {0: "router blk0 start", 1: "router blk0 setup done", 2: "router blk0 fi
 
 def tiny_items(lib, t0, layer):
     """Per-CTA work-item timeline of k_experts_tiny (us from the router start):
-    id claimed | dependency met | last TMA issued | epilogue done."""
-    C, N, F = 160, 8, 5
+    id claimed | dependency met | last TMA issued | epilogue done | first MMA | last MMA | acc to epilogue |
+    k-block n-2 ready | k-block n-1 ready."""
+    C, N, F = 160, 8, 10
     buf = (ctypes.c_ulonglong * (C * N * F))()
     lib.lp_trace_items.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.lp_trace_items(buf, C * N * F)
@@ -51,7 +52,7 @@ def tiny_items(lib, t0, layer):
                 continue
             us = [(v - t0) / 1000 if v else float("nan") for v in f[1:]]
             kind = "?" if n_up is None else ("U" if f[0] < n_up else ("D" if f[0] < n_up + 16 * hit else "end"))
-            items.append(f"{kind}{f[0]}:{us[0]:.1f}/{us[1]:.1f}/{us[2]:.1f}/{us[3]:.1f}")
+            items.append(f"{kind}{f[0]}:" + "/".join(f"{u:.1f}" for u in us))
             if kind == "U":
                 ups.append(us)
             elif kind == "D":
