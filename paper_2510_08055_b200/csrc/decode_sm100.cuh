@@ -96,6 +96,7 @@ struct DecodeParams {
   int weights_evict_first;
   int warm_w2;             // 1: L2-prefetch the hit experts' W2 when small
   int dnc;                 // 1: block-diagonal DN + combine items when S <= 16 and every UP item fits one wave
+  int act_gather;          // 1: DN items' act rows copied by the gather warps (cp.async) instead of TMA
 };
 
 __device__ __forceinline__ void cluster_arrive_rel() {
@@ -449,7 +450,18 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
           const int kblocks = p.I / kTileK;
           const int npre = kblocks < S_ ? kblocks : S_;
           const int st0 = stage;
-          for (int kb = 0; kb < kblocks; ++kb) {
+          if (p.act_gather) {  // the gather warps bring the act rows: weights only, no dependency here
+            LP_ITEM(n_item, 2, LP_NOW());
+            for (int kb = 0; kb < kblocks; ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sa = smem + stage * C::kStageBytes;
+              mbar_arrive_expect_tx(&full[stage], abytes);
+              for (int j = 0; j < nnz; ++j)
+                tma_load_2d(sa + j * rdnc * 128, tmr, &full[stage], kb * kTileK, s_hit[j] * p.H + m0, pol_w);
+              if (++stage == S_) { stage = 0; phase ^= 1; }
+            }
+          }
+          for (int kb = 0; kb < (p.act_gather ? 0 : kblocks); ++kb) {
             if (kb == npre) {
               while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
               fence_proxy_async_global();
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
             if (kb >= npre) tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, 0, pol_a);
             if (++stage == S_) { stage = 0; phase ^= 1; }
           }
-          if (npre == kblocks) {  // every k-block fitted the ring: the act rows follow the dependency
+          if (!p.act_gather && npre == kblocks) {  // every k-block fitted the ring: act rows follow the dependency
             while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
             fence_proxy_async_global();
             LP_ITEM(n_item, 2, LP_NOW());
@@ -475,6 +487,15 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
               tma_load_2d(smem + s2 * C::kStageBytes + kATileBytes, &tm_act, &full[s2], k2 * kTileK, 0, pol_a);
               if (++s2 == S_) s2 = 0;
             }
+          }
+        } else if (p.act_gather) {
+          // W2 tiles only: the gather warps copy expert e's act rows once its UP items are done
+          LP_ITEM(n_item, 2, LP_NOW());
+          for (int kb = 0; kb < p.I / kTileK; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], kATileBytes);
+            tma_load_2d(smem + stage * C::kStageBytes, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
+            if (++stage == S_) { stage = 0; phase ^= 1; }
           }
         } else {
           // W2 tiles first (they do not depend on the UP items), the act rows once expert e's act is final
@@ -579,6 +600,28 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
 #pragma unroll
           for (int i = 0; i < RPT; ++i)
             if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
+          cp_async_arrive_noinc(&bfull[stage]);
+          cp_async_commit();
+          if (++stage == S_) { stage = 0; phase ^= 1; }
+        }
+      } else if (p.act_gather) {
+        // DN / DNC items: this item's act rows [row0, row0 + nvalid) once the UP items they need are done
+        // (expert e's for DN, every expert's for DNC), 16-byte cp.async into the SWIZZLE_128B B stage
+        const int row0 = info.z, nvalid = info.w;
+        // every lane acquires (its own cp.async reads are ordered after its own acquire)
+        if (kind == kItemDnc)
+          while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
+        else
+          while (ld_acquire_u32(&p.sched[1 + (info.x >> 8)]) < static_cast<uint32_t>(mt_up)) __nanosleep(32);
+        const __nv_bfloat16* as = p.act + static_cast<size_t>(row0) * p.I + j * 8;
+        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
+        for (int kb = 0; kb < p.I / kTileK; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          cp_async_wait_group<S_ - 1>();
+          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + kATileBytes) + sw;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+            if (g + 8 * i < nvalid) cp_async16(sb + i * 8 * 128, as + static_cast<size_t>(g + 8 * i) * p.I + kb * kTileK, pol_x);
           cp_async_arrive_noinc(&bfull[stage]);
           cp_async_commit();
           if (++stage == S_) { stage = 0; phase ^= 1; }

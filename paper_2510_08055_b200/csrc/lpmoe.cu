@@ -577,7 +577,11 @@ int launch_experts_tiny(const void* x, const int32_t* tok_of, int S, const void*
 // Decode-size layers (T <= 16, T*topk <= E <= 128, H % 256 == 0) run router,
 // permutation and the expert stream in ONE launch (decode_sm100.cuh), bit-
 // identical to k_router<4, 4, 16> + k_scan_slots + k_experts_tiny. LPMOE_DECODE=0
-// disables; LPMOE_DECODE_W2_WARM=0 turns off its L2 warm-up of the hit experts' W2.
+// disables. Knobs (B200, T=1 / 2 / 8 layer us, profiles/r02): LPMOE_DECODE_W2_WARM=1 L2-warms the hit
+// experts' W2 during the UP phase (off: 32.3 vs 34.2 at T=1 — it competes with the UP stream);
+// LPMOE_DECODE_DNC=0 disables the block-diagonal DN+combine items (on: 31.0 vs 31.9 at T=1);
+// LPMOE_DECODE_ACT_GATHER=0 loads DN act rows by TMA after the dependency instead of cp.async by
+// the gather warps (gather: 31.0 / 41.6 / 86.7 vs 32.8 / 41.9 / 91.7).
 bool use_decode(int T, int H, int I, int E, int topk) {
   static const int v = env_int("LPMOE_DECODE", 1);
   return v != 0 && T >= 1 && T <= lp::DecodeCfg::kMaxT && T * topk <= E && E <= lp::DecodeCfg::kMaxE &&
@@ -588,8 +592,9 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
                   int topk, int renorm, int32_t* ids, float* w, int32_t* counts, int32_t* offsets, int32_t* slot_of,
                   int32_t* tok_of, void* act, void* y_perm, uint32_t* sched, void* y, uint32_t* cmb, int wpol,
                   cudaStream_t st) {
-  static const int warm = env_int("LPMOE_DECODE_W2_WARM", 1);
+  static const int warm = env_int("LPMOE_DECODE_W2_WARM", 0);
   static const int dnc = env_int("LPMOE_DECODE_DNC", 1);
+  static const int act_gather = env_int("LPMOE_DECODE_ACT_GATHER", 1);
   int rc;
   if ((rc = get_encode())) return rc;
   const int S = T * topk;
@@ -611,7 +616,8 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
   const lp::DecodeParams p{T, H, I, E, topk, renorm, static_cast<const __nv_bfloat16*>(x),
                            static_cast<const uint8_t*>(w2), ids, w, counts, offsets, slot_of, tok_of,
                            static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0, dnc != 0 ? 1 : 0};
+                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0, dnc != 0 ? 1 : 0,
+                           act_gather != 0 ? 1 : 0};
   // clusters of 4 that are co-resident (GPC boundaries can leave SMs that no 4-CTA cluster fits):
   // a second wave would repeat the routing prologue after the first wave's stream
   static std::mutex mu;
