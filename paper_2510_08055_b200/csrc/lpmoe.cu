@@ -1120,6 +1120,7 @@ int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, co
   if (T == 0) return ok();
   if (!x || !ids || !slot_of || !offsets || !dest_base || !peer_recv || !dest_rank || !dest_row)
     return fail(LP_EINVAL, "lp_ep_dispatch: null pointer argument");
+  if (!aligned16(x)) return fail(LP_EINVAL, "lp_ep_dispatch: x must be 16-byte aligned");
   const int S = T * topk;
   count_launch();
   lp::k_ep_dispatch<<<(S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -1134,6 +1135,7 @@ int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* 
   if (T < 0 || H <= 0 || H % 8 || topk < 1 || topk > 32) return fail(LP_EINVAL, "lp_ep_combine: bad shape");
   if (T == 0) return ok();
   if (!peer_y || !dest_rank || !dest_row || !w || !y) return fail(LP_EINVAL, "lp_ep_combine: null pointer argument");
+  if (!aligned16(y)) return fail(LP_EINVAL, "lp_ep_combine: y must be 16-byte aligned");
   count_launch();
   lp::k_ep_combine<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,

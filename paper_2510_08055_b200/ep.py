@@ -245,9 +245,17 @@ class PeerRegion:
         self.recv_x_ptr = self.base + off_recv  # [cap, H] bf16
         self.y_out_ptr = self.base + off_y      # [cap, H] bf16
         self._act: torch.Tensor | None = None
+        self._ws: torch.Tensor | None = None
         self.dest_base = torch.empty((world * el,), dtype=torch.int32, device=device)
         self.off_local = torch.empty((el + 1,), dtype=torch.int32, device=device)
         dist.barrier(group=group)  # every rank mapped every region before the first device barrier
+
+    def workspace(self, need: int) -> torch.Tensor:
+        """The stack's shared liblpmoe workspace (zeroed once: every call leaves its header zeroed).
+        Grows only while layers are being built; a captured graph keeps the final address."""
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._ws
 
     def act(self, ffn: int) -> torch.Tensor:
         """Local [cap, ffn] bf16 scratch for the experts' SiLU(g)*u rows (shared by the stack)."""
@@ -332,7 +340,8 @@ class PeerEP:
         self._recv_rows = torch.zeros((1,), dtype=torch.int32, device=dev)
         need = max(int(self.lib.lp_moe_workspace_bytes(max_tokens, H, 128, E, k)),   # route + permute
                    int(self.lib.lp_moe_workspace_bytes(1, H, shape.ffn, self.el, 1)))  # expert tile plan
-        self._ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        self._ws_need = need
+        region.workspace(need)  # one scratch per stack: its layers run in sequence on one stream
 
     @classmethod
     def from_full(cls, shape: MoEShape, wr, w13, w2, rank: int, world: int, max_tokens: int, group=None,
@@ -352,7 +361,7 @@ class PeerEP:
         require(T <= self.max_tokens, f"T={T} exceeds max_tokens={self.max_tokens}")
         _check_tensor("x", x, (T, H), torch.bfloat16)
         st = _stream_ptr(self.device)
-        ws = self._ws
+        ws = rg.workspace(self._ws_need)
         # (pointers from the full buffers: an empty view's data_ptr() is 0, which the ABI rejects)
         ids, w, counts = self._ids[:T], self._w[:T], self._counts
         mark(0)

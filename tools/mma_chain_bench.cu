@@ -21,6 +21,7 @@ using namespace lp;
 
 template <int N, int NACC, int COMMIT = 0, int SPIN = 0>
 __global__ void __launch_bounds__(256, 1) k_chain(int kblocks, unsigned long long* out) {
+  const uint32_t* gflag = reinterpret_cast<const uint32_t*>(out + 4);  // a zero word in global memory
   extern __shared__ uint8_t raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   constexpr int kA = 16384, kB = N * 128;
@@ -56,6 +57,13 @@ __global__ void __launch_bounds__(256, 1) k_chain(int kblocks, unsigned long lon
       if (COMMIT == 2 || COMMIT == 4) { mbar_wait(&ring[8 + (kb & 7)], 0); mbar_wait(&ring[8 + ((kb + 1) & 7)], 0); }
       if (COMMIT == 3 || COMMIT == 5) mbar_wait(&ring[8 + (kb & 7)], 0);
       if (COMMIT == 2 || COMMIT == 3) tc_fence_after();
+      if (COMMIT == 10) mbar_wait(&ring[8 + (kb & 7)], 0);  // wait per k-block, NO commit
+      if (COMMIT == 11) {  // poll a GLOBAL word (LDG) per k-block, then commit
+        uint32_t v;
+        do {
+          asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(gflag) : "memory");
+        } while (v != 0u);
+      }
       if (COMMIT == 9) {  // relaxed volatile LDS poll, no fence
         uint32_t v;
         do {
@@ -71,7 +79,7 @@ __global__ void __launch_bounds__(256, 1) k_chain(int kblocks, unsigned long lon
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb >= NACC) || k != 0);
-      if ((COMMIT >= 1 && COMMIT <= 5) || COMMIT >= 8) mma_commit(&ring[kb & 7]);
+      if ((COMMIT >= 1 && COMMIT <= 5) || COMMIT == 8 || COMMIT == 9 || COMMIT == 11) mma_commit(&ring[kb & 7]);
       // 6: one wait + one commit per PAIR of k-blocks; 7: two waits + two commits per pair (per-stage release)
       if (COMMIT == 6 && (kb & 1)) { mma_commit(&ring[kb & 7]); mbar_wait(&ring[8 + (kb & 7)], 0); }
       if (COMMIT == 7 && (kb & 1)) {
@@ -121,6 +129,7 @@ void run(int kblocks, unsigned long long* d_out) {
 int main() {
   unsigned long long* d_out;
   CK(cudaMalloc(&d_out, 64));
+  CK(cudaMemset(d_out, 0, 64));
   for (int kb : {12, 32, 128}) {
     run<16, 1>(kb, d_out);
     run<16, 2>(kb, d_out);
@@ -133,6 +142,12 @@ int main() {
   run<16, 1, 5>(32, d_out);
   run<16, 1, 8>(32, d_out);
   run<16, 1, 9>(32, d_out);
+  run<16, 1, 10>(32, d_out);
+  run<16, 1, 11>(32, d_out);
+  run<64, 2, 2>(32, d_out);
+  run<128, 1, 2>(32, d_out);
+  run<256, 1, 2>(32, d_out);
+  run<256, 1, 1>(32, d_out);
   run<16, 1, 6>(32, d_out);
   run<16, 1, 7>(32, d_out);
   run<16, 1, 2, 1>(32, d_out);  // + 7 other warps spinning on an mbarrier (try_wait loops)
