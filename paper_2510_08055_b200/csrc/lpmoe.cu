@@ -465,12 +465,18 @@ int launch_scan_scatter(const int32_t* ids, const void* x, int T, int H, int E, 
   const int nchunks = (T + chunk_tokens - 1) / chunk_tokens;
   const int n_hist = nchunks * E;
   const int smem = n_hist <= lp::kScanSmemInts ? n_hist * 4 : 0;
-  if (smem > 48 * 1024) {
+  // opt in whenever dynamic + static (s_part, 4 KiB) may pass the 48 KiB default (cached per device)
+  if (smem > 0) {
     int rc;
     if ((rc = set_smem(lp::k_scan, lp::kScanSmemInts * 4))) return rc;
   }
-  LP_CUDA(launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts, offsets,
-                     tile_prefix, tile_rows, sched, zero_buf, zero_n));
+  {
+    const cudaError_t e = launch_pdl(lp::k_scan, 1, lp::kScanThreads, smem, st, chunk_hist, nchunks, E, max_n, counts,
+                                     offsets, tile_prefix, tile_rows, sched, zero_buf, zero_n);
+    if (e != cudaSuccess)
+      return fail(LP_ECUDA, "k_scan launch (T=%d nchunks=%d E=%d smem=%d): %s", T, nchunks, E, smem,
+                  cudaGetErrorString(e));
+  }
   if (x_perm == nullptr) {
     LP_CUDA(launch_pdl(lp::k_slots, (S + 255) / 256, 256, 0, st, ids, static_cast<const int32_t*>(chunk_hist),
                        rank_local, static_cast<const int32_t*>(offsets), S, E, topk, chunk_tokens * topk, slot_of,

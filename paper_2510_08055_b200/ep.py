@@ -371,7 +371,7 @@ class PeerEP:
                           "lp_moe_route")
         _native.check(lib.lp_moe_permute(self._ids.data_ptr(), x.data_ptr(), T, H, E, k, counts.data_ptr(),
                                          self._offsets.data_ptr(), self._slot_of.data_ptr(), self._tok_of.data_ptr(),
-                                         None, ws.data_ptr(), ws.numel(), st), "lp_moe_permute")
+                                         None, ws.data_ptr(), ws.numel(), st), f"lp_moe_permute (T={T})")
         mark(1)
         rg.exchange(counts, st)  # counts to every rank + wait for every source + plan (one launch)
         _native.check(lib.lp_ep_dispatch(x.data_ptr(), self._ids.data_ptr(), self._slot_of.data_ptr(),

@@ -73,11 +73,13 @@ def test_tiny_config(cuda, T):
     check_layer(TINY, T, 11, cuda)
 
 
-@pytest.mark.parametrize("T", [1, 8, 32, 64, 576, 1000, 2048, 8224])
+@pytest.mark.parametrize("T", [1, 8, 32, 64, 576, 1000, 2048, 5784, 8224])
 def test_qwen_layer(cuda, T):
     # 576 = BASELINE config 2 (64 decode + 512 prefill); 32 = decode-only layer of config 3;
     # 8224 = config 3's designated-group batch (8192 prompt + 32 decodes: CTA-pair kernel on the
-    # materialised x_perm); 2048 = between the memory-bound and compute-bound regimes
+    # materialised x_perm); 2048 = between the memory-bound and compute-bound regimes; 5784 = the
+    # scan's tile histograms take 46.5 KiB of dynamic shared memory (+ 4 KiB static: needs the
+    # opt-in below 48 KiB of dynamic — found by the EP serving run)
     err, stats, ref = check_layer(QWEN3_30B_A3B, T, 21, cuda)
     if T >= 576:
         assert stats.experts_hit == 128
@@ -164,7 +166,7 @@ def test_staged_api_matches_fused(cuda):
     assert mo.rel_l2(y_perm.float().cpu().numpy(), ref["y_perm"]) <= REL_L2_TOL
 
 
-@pytest.mark.parametrize("T", [1, 37, 576, 2500, 8224])
+@pytest.mark.parametrize("T", [1, 37, 576, 2500, 5784, 8224])
 def test_permute_slot_maps_without_rows(cuda, T):
     """Index-only permutation (one fused scan + slot-map launch) = the oracle's stable counting sort."""
     s = QWEN3_30B_A3B
