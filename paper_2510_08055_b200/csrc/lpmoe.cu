@@ -616,7 +616,9 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
     if ((rc = make_tmap(&tm_w2r[i], w2, static_cast<uint64_t>(E) * H, I, 8u << i))) return rc;
   constexpr int smem = lp::DecodeCfg::kSmemBytes;
   static const int forced_cs = env_int("LPMOE_DECODE_CS", 0);
-  const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 4 ? 4 : 2);
+  // B200 (profiles/r02/decode_cs.jsonl): 4-CTA clusters (132 SMs, half the Wr bytes per CTA) win at T <= 3
+  // (T=1 30.6 vs 33.2 us, T=2 41.2 vs 44.5), pairs (148 SMs streaming) from T=4 (58.3 vs 60.1)
+  const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 3 ? 4 : 2);
   auto kern = cs == 4 ? lp::k_decode<4> : lp::k_decode<2>;
   if ((rc = set_smem(kern, smem))) return rc;
   const lp::DecodeParams p{T, H, I, E, topk, renorm, static_cast<const __nv_bfloat16*>(x),
