@@ -215,7 +215,29 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, C::kN);
-      for (int i = 0; i < kbr; ++i) {  // partial (i / kbp) accumulates in TMEM columns 16 * (i / kbp)
+      if (kbr <= S_) {
+        // every routing k-block fits the ring (all loads already in flight): wait for all of them,
+        // then issue the whole MMA chain back to back — a stage wait after an MMA issue costs the
+        // issuing thread ~250 cycles (tools/mma_chain_bench.cu), so no wait sits between MMAs.
+        // Same MMAs in the same order as below (bit-identical logits).
+        for (int i = 0; i < kbr; ++i) {
+          mbar_wait(&full[i], 0);
+          mbar_wait(&bfull[i], 0);
+        }
+        tc_fence_after();
+        for (int i = 0; i < kbr; ++i) {
+          const uint32_t sa = smem_u32(smem + i * C::kStageBytes);
+          const uint64_t a0 = sdesc_kmajor_sw128(sa);
+          const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
+          const uint32_t d = tmem_base + (i / kbp) * C::kN;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((i % kbp) | k) != 0);
+        }
+        for (int i = 0; i < kbr; ++i) mma_commit(&empty[i]);
+        stage = kbr % S_;
+        phase = kbr == S_ ? 1u : 0u;
+      }
+      for (int i = 0; i < (kbr <= S_ ? 0 : kbr); ++i) {  // partial (i / kbp) accumulates in TMEM columns 16 * (i / kbp)
         mbar_wait(&full[stage], phase);
         mbar_wait(&bfull[stage], phase);
         tc_fence_after();
