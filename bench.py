@@ -150,13 +150,13 @@ def measured_tensor_peak():
     return 2250.0, "fallback (nominal dense bf16 2.25 PF/s)"
 
 
-def ncu_traffic(T: int):
-    """DRAM bytes per k_experts launch at this T from the latest committed `ncu --set full`
-    capture (profiles/rNN/k_experts_traffic.json, written by tools/summarize_evidence.py)."""
+def ncu_traffic(T: int, kernel: str = "k_experts"):
+    """DRAM bytes per launch of the dominant kernel at this T from the latest committed `ncu --set
+    full` capture (profiles/rNN/k_experts_traffic.json, written by tools/summarize_evidence.py)."""
     import glob
 
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k_experts_traffic.json")), reverse=True):
-        d = json.load(open(path)).get(f"k_experts_{T}")
+        d = json.load(open(path)).get(f"{kernel}_{T}")
         if d:
             return d["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
     return None, None
@@ -458,8 +458,10 @@ def run_ours(args, rank: int, world: int):
         # single GPU (gather regime): the kernel reads each token row from x once and writes y_perm rows
         # at slot granularity; with EP the rows it reads are the received ones
         algo_bytes = nnz * s.bytes_per_expert + (2 * T * s.hidden * 2 if world == 1 else 2 * R * s.hidden * 2)
-        achieved = algo_bytes / (stage_us["experts"] * 1e-6) / 1e9
-        traffic, traffic_src = ncu_traffic(T)
+        t_kernel = stage_us["experts"]
+        achieved = algo_bytes / (t_kernel * 1e-6) / 1e9
+        decode = world == 1 and n_launches == K  # one launch per step: the fused decode-size kernel ran
+        traffic, traffic_src = ncu_traffic(T, "k_decode" if decode else "k_experts")
         if traffic_src:
             traffic_src += " (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         layer_bytes = nnz * s.bytes_per_expert + s.num_experts * s.hidden * 2 + 2 * T * s.hidden * 2 + T * s.top_k * 8
@@ -467,9 +469,13 @@ def run_ours(args, rank: int, world: int):
         tpeak, tpeak_src = measured_tensor_peak()
         kernel = ("k_experts / k_experts_pair (grouped gate/up+SiLU*mul and down, tcgen05); duration from CUDA "
                   "events around its launch in a second pass over the same K steps")
+        if decode:
+            kernel = ("k_decode (the whole decode-size layer in one launch: routing, permutation, expert stream, "
+                      "combine); duration from CUDA events around it in a second pass over the same K steps")
+            stage_us = {"decode_kernel": stage_us["experts"]}
         if flops / algo_bytes > tpeak * 1e12 / (peak * 1e9):
             # arithmetic intensity above the measured ridge: the expert kernel is tensor-bound
-            tf = flops / (stage_us["experts"] * 1e-6) / 1e12
+            tf = flops / (t_kernel * 1e-6) / 1e12
             out["roofline"] = {"bound": "tensor", "kernel": kernel, "achieved": tf, "peak": tpeak, "unit": "TFLOP/s",
                                "frac": tf / tpeak, "traffic": traffic, "traffic_source": traffic_src,
                                "peak_source": tpeak_src, "algo_flops_per_launch": flops,

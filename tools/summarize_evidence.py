@@ -54,7 +54,7 @@ def main():
             for m, v, u in ms:
                 lines.append(f"  {m:70s} {v:>16s} {u}")
                 vals[m] = (v, u)
-            if "k_experts" in kern:
+            if "k_experts" in kern or "k_decode" in kern:
                 def to_bytes(v, u):
                     f = float(v.replace(",", ""))
                     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
@@ -67,7 +67,7 @@ def main():
     with open(os.path.join(dst, "k_experts_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     for fn in ("bench.jsonl", "bench_ref.jsonl", "bench_sweep.jsonl", "serving_c3.jsonl", "serving_c4.jsonl",
-               "serving_c5.jsonl", "pytest_gpu.log", "smoke.log", "trace_T576.txt", "k_experts_576.ncu-rep"):
+               "serving_c5.jsonl", "pytest_gpu.log", "smoke.log", "trace_T576.txt"):
         p = os.path.join(ev, fn)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(dst, fn))
