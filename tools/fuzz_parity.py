@@ -29,7 +29,7 @@ def main():
     fails = 0
     for i in range(n):
         s = SHAPES[int(rng.integers(len(SHAPES)))]
-        T = int(rng.choice([1, 2, 7, 33, 64, 100, 255, 576, 1000, 1553, 2048, 3001, 4100, 6000, 8224]))
+        T = int(rng.choice([1, 2, 3, 4, 5, 8, 16, 7, 33, 64, 100, 255, 576, 1000, 1553, 2048, 3001, 4100, 5784, 6000, 8224]))
         if s.hidden * s.ffn > 4_000_000 and T > 4100:
             T = 4100  # keep the fp32 oracle quick on the large shapes
         skew = bool(rng.integers(2))
