@@ -165,9 +165,10 @@ int lp_ep_barrier(uint32_t* const* peer_ctl, int P, int rank, void* stream);
  * is in this rank's block: dest_base[d*El+el] = first row of this rank's
  * entries for expert el in rank d's receive buffer (rows expert-major,
  * source-rank-major within an expert); off_local[0..El] = this rank's expert
- * offsets over all sources (off_local[El] = rows received). */
+ * offsets over all sources (off_local[El] = rows received; also stored to
+ * *rows_out when rows_out is not NULL: off_local is rewritten by the next layer). */
 int lp_ep_exchange(const int32_t* counts, uint32_t* const* peer_ctl, int P, int El, int rank, int32_t* dest_base,
-                   int32_t* off_local, void* stream);
+                   int32_t* off_local, int32_t* rows_out, void* stream);
 
 /* Fused permute + dispatch: entry i = t*topk + j (ids/slot_of/offsets from
  * lp_moe_route + lp_moe_permute over the P*El global experts) stores x[t]

@@ -49,7 +49,7 @@ SIGNATURES = {
     "lp_ipc_close": (_i, [_p]),
     "lp_ep_ctl_bytes": (_sz, [_i, _i]),
     "lp_ep_barrier": (_i, [_p, _i, _i, _p]),
-    "lp_ep_exchange": (_i, [_p, _p, _i, _i, _i, _p, _p, _p]),
+    "lp_ep_exchange": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, _p]),
     "lp_ep_dispatch": (_i, [_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _p, _p, _p]),
     "lp_ep_combine": (_i, [_p, _p, _p, _p, _i, _i, _i, _p, _p]),
 }

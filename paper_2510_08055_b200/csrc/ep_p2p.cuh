@@ -29,6 +29,7 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
+#include "ptx.cuh"
 
 namespace lp {
 
@@ -40,6 +41,13 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
   return v;
 }
+// Spin with relaxed system-scope polls, then one acquire fence (an acquire per poll is slower)
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 // Per-rank control block (the first lp_ep_ctl_bytes(P, E) bytes of a rank's region):
 //   u32 [0]  barrier counter (peers add to it)      u32 [1]  barriers this rank passed (own)
@@ -53,15 +61,19 @@ constexpr int kEpMaxRanks = 32;
 // far, kept on the device in ctl[1], so a captured CUDA graph replays correctly). Counters only
 // grow; no rank can arrive at barrier n+1 before every rank arrived at barrier n.
 __global__ void k_ep_barrier(uint32_t* const* __restrict__ peer_ctl, int P, int rank) {
+  pdl_trigger();  // (PDL: the next kernel's prologue may start; it waits for this grid before its data)
+  pdl_wait();
   const int lane = threadIdx.x;
   uint32_t* mine = peer_ctl[rank];
-  __threadfence_system();
+  if (lane == 0) __threadfence_system();  // the preceding kernels' peer stores, before the release adds
   __syncwarp();
   for (int q = lane; q < P; q += 32) red_add_release_sys(peer_ctl[q], 1u);
   if (lane == 0) {
     const uint32_t n = mine[1] + 1u;
     const uint32_t target = static_cast<uint32_t>(P) * n;
-    while (static_cast<int32_t>(ld_acquire_sys(mine) - target) < 0) __nanosleep(64);
+    while (static_cast<int32_t>(ld_relaxed_sys(mine) - target) < 0) {
+    }
+    fence_acq_rel_sys();
     mine[1] = n;
   }
   __syncwarp();
@@ -82,7 +94,10 @@ __device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
 // exchange of layer n+1 saw every peer's tag n+2, which each peer posts after planning layer n.
 __global__ void __launch_bounds__(1024)
     k_ep_exchange(const int32_t* __restrict__ counts, uint32_t* const* __restrict__ peer_ctl, int P, int El,
-                  int rank, int32_t* __restrict__ dest_base, int32_t* __restrict__ off_local) {
+                  int rank, int32_t* __restrict__ dest_base, int32_t* __restrict__ off_local,
+                  int32_t* __restrict__ rows_out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ int32_t s_cnt[];  // [P src][E]
   __shared__ uint32_t s_layer;
   const int E = P * El;
@@ -96,31 +111,60 @@ __global__ void __launch_bounds__(1024)
     const int d = i / E, e = i - d * E;
     reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(peer_ctl[d]) + kCtlInbox)[box + e] = counts[e];
   }
-  __threadfence_system();
+  // one system-scope fence after the CTA barrier publishes every thread's inbox stores (cumulativity);
+  // a fence per thread cost ~35 us per launch
   __syncthreads();
-  if (threadIdx.x < P) st_release_sys(peer_ctl[threadIdx.x] + kCtlReadyWord + parity * kEpMaxRanks + rank, layer + 1u);
-  if (threadIdx.x < P) {
+  if (threadIdx.x == 0) __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < P && threadIdx.x != rank)
+    st_release_sys(peer_ctl[threadIdx.x] + kCtlReadyWord + parity * kEpMaxRanks + rank, layer + 1u);
+  if (threadIdx.x < P && threadIdx.x != rank) {  // (this rank's own counts: ordered by the CTA barrier)
     const uint32_t* tag = mine + kCtlReadyWord + parity * kEpMaxRanks + threadIdx.x;
-    while (ld_acquire_sys(tag) != layer + 1u) __nanosleep(32);
+    while (ld_relaxed_sys(tag) != layer + 1u) {
+    }
+    fence_acq_rel_sys();
   }
   __syncthreads();
   const int32_t* inbox = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(mine) + kCtlInbox) +
                          static_cast<size_t>(parity) * P * E;
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) s_cnt[i] = __ldcv(inbox + i);  // L1 may hold layer n-2
   __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) {
-    const int d = i / El;
-    int base = 0;
-    for (int e2 = d * El; e2 < i; ++e2)
-      for (int s = 0; s < P; ++s) base += s_cnt[s * E + e2];
-    for (int s = 0; s < rank; ++s) base += s_cnt[s * E + i];
-    dest_base[i] = base;
+  // plan with one block-wide scan (E <= 256 = blockDim experts): tot[e] = rows of expert e over all
+  // sources; incl[e] = inclusive prefix of tot; the prefix within owner d's block of El experts is
+  // incl[e] - tot[e] - incl[d*El - 1]
+  __shared__ int32_t s_incl[256];
+  __shared__ int32_t s_warp[8];
+  const int t = threadIdx.x;
+  int tot = 0, before = 0;
+  if (t < E) {
+    for (int s2 = 0; s2 < P; ++s2) {
+      const int c = s_cnt[s2 * E + t];
+      tot += c;
+      if (s2 < rank) before += c;
+    }
   }
-  for (int i = threadIdx.x; i <= El; i += blockDim.x) {  // El + 1 entries
-    int o = 0;
-    for (int e2 = rank * El; e2 < rank * El + i; ++e2)
-      for (int s = 0; s < P; ++s) o += s_cnt[s * E + e2];
-    off_local[i] = o;
+  int incl = tot;
+  const int lane = t & 31, wid = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  for (int w2 = 0; w2 < wid; ++w2) incl += s_warp[w2];
+  if (t < E) s_incl[t] = incl;
+  __syncthreads();
+  if (t < E) {
+    const int d = t / El;
+    const int blk0 = d * El > 0 ? s_incl[d * El - 1] : 0;
+    const int excl_blk = incl - tot - blk0;  // rows of experts d*El .. t-1 (all sources)
+    dest_base[t] = excl_blk + before;
+    if (d == rank) off_local[t - rank * El] = excl_blk;
+    if (t == (rank + 1) * El - 1) {
+      off_local[El] = incl - blk0;
+      if (rows_out != nullptr) *rows_out = incl - blk0;  // the caller's copy (off_local is rewritten next layer)
+    }
   }
   if (threadIdx.x == 0) mine[2] = layer + 1u;
 }
@@ -133,6 +177,8 @@ __global__ void __launch_bounds__(256)
                   const int32_t* __restrict__ slot_of, const int32_t* __restrict__ offsets,
                   const int32_t* __restrict__ dest_base, __nv_bfloat16* const* __restrict__ peer_recv, int S, int H,
                   int topk, int El, int32_t* __restrict__ dest_rank, int32_t* __restrict__ dest_row) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (i < S) {
@@ -147,7 +193,8 @@ __global__ void __launch_bounds__(256)
     uint4* dst = reinterpret_cast<uint4*>(peer_recv[d] + static_cast<size_t>(row) * H);
     for (int v = lane; v < H / 8; v += 32) dst[v] = src[v];
   }
-  __threadfence_system();
+  __syncthreads();  // one fence per CTA (after the barrier) instead of one per thread
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 // CTA per token: y[t] = sum_j w[t,j] * y_out_{dest_rank}[dest_row] (fp32, fixed j order), with
@@ -157,6 +204,8 @@ __global__ void __launch_bounds__(256)
     k_ep_combine(__nv_bfloat16* const* __restrict__ peer_y, const int32_t* __restrict__ dest_rank,
                  const int32_t* __restrict__ dest_row, const float* __restrict__ w, int T, int topk, int H,
                  __nv_bfloat16* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   __shared__ const uint4* s_row[32];
   __shared__ float s_w[32];

@@ -1101,23 +1101,21 @@ int lp_ep_barrier(uint32_t* const* peer_ctl, int P, int rank, void* stream) {
   if (P < 1 || P > lp::kEpMaxRanks || rank < 0 || rank >= P || !peer_ctl)
     return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
   count_launch();
-  lp::k_ep_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(peer_ctl, P, rank);
-  LP_CHECK_LAUNCH("k_ep_barrier");
+  LP_CUDA(launch_pdl(lp::k_ep_barrier, 1, 32, 0, static_cast<cudaStream_t>(stream), peer_ctl, P, rank));
   return ok();
 }
 
 int lp_ep_exchange(const int32_t* counts, uint32_t* const* peer_ctl, int P, int El, int rank, int32_t* dest_base,
-                   int32_t* off_local, void* stream) {
+                   int32_t* off_local, int32_t* rows_out, void* stream) {
   if (P < 1 || P > lp::kEpMaxRanks || El < 1 || P * El > lp::kMaxExperts || rank < 0 || rank >= P || !counts ||
       !peer_ctl || !dest_base || !off_local)
     return fail(LP_EINVAL, "lp_ep_exchange: bad arguments P=%d El=%d rank=%d", P, El, rank);
   const size_t sm = static_cast<size_t>(P) * P * El * sizeof(int32_t);
   if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_exchange: P*P*El too large");
   count_launch();
-  const int threads = P * El + 1 > 256 ? 512 : 256;  // >= El + 1 not required (strided), >= P is
-  lp::k_ep_exchange<<<1, threads, sm, static_cast<cudaStream_t>(stream)>>>(counts, peer_ctl, P, El, rank,
-                                                                          dest_base, off_local);
-  LP_CHECK_LAUNCH("k_ep_exchange");
+  const int threads = 256;  // one thread per global expert (P * El <= 256) for the plan's block scan
+  LP_CUDA(launch_pdl(lp::k_ep_exchange, 1, threads, sm, static_cast<cudaStream_t>(stream), counts, peer_ctl, P, El,
+                     rank, dest_base, off_local, rows_out));
   return ok();
 }
 
@@ -1131,10 +1129,9 @@ int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, co
   if (!aligned16(x)) return fail(LP_EINVAL, "lp_ep_dispatch: x must be 16-byte aligned");
   const int S = T * topk;
   count_launch();
-  lp::k_ep_dispatch<<<(S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), ids, slot_of, offsets, dest_base,
-      reinterpret_cast<__nv_bfloat16* const*>(peer_recv), S, H, topk, El, dest_rank, dest_row);
-  LP_CHECK_LAUNCH("k_ep_dispatch");
+  LP_CUDA(launch_pdl(lp::k_ep_dispatch, (S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream),
+                     static_cast<const __nv_bfloat16*>(x), ids, slot_of, offsets, dest_base,
+                     reinterpret_cast<__nv_bfloat16* const*>(peer_recv), S, H, topk, El, dest_rank, dest_row));
   return ok();
 }
 
@@ -1145,10 +1142,9 @@ int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* 
   if (!peer_y || !dest_rank || !dest_row || !w || !y) return fail(LP_EINVAL, "lp_ep_combine: null pointer argument");
   if (!aligned16(y)) return fail(LP_EINVAL, "lp_ep_combine: y must be 16-byte aligned");
   count_launch();
-  lp::k_ep_combine<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,
-      static_cast<__nv_bfloat16*>(y));
-  LP_CHECK_LAUNCH("k_ep_combine");
+  LP_CUDA(launch_pdl(lp::k_ep_combine, T, 256, 0, static_cast<cudaStream_t>(stream),
+                     reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,
+                     static_cast<__nv_bfloat16*>(y)));
   return ok();
 }
 

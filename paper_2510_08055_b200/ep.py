@@ -104,7 +104,7 @@ class GpuOps:
 class EPStats:
     counts: torch.Tensor       # int32 [E] global-expert counts of this rank's tokens
     recv_rows: "int | torch.Tensor"    # rows this rank's experts processed (PeerEP: a device scalar, no sync)
-    send_splits: "list[int] | torch.Tensor"
+    send_splits: "list[int] | None"      # EPMoE: rows sent per rank; PeerEP: None (counts.view(P, El).sum(1))
     recv_splits: list[int]
     shape: MoEShape
 
@@ -268,12 +268,13 @@ class PeerRegion:
         _native.check(self.lib.lp_ep_barrier(self.peer_ctl.data_ptr(), self.world, self.rank, stream),
                       "lp_ep_barrier")
 
-    def exchange(self, counts: torch.Tensor, stream) -> None:
+    def exchange(self, counts: torch.Tensor, stream, rows_out: torch.Tensor | None = None) -> None:
         """Post this rank's per-global-expert counts to every rank, wait for every source's, plan
-        dest_base / off_local (one launch)."""
+        dest_base / off_local (one launch); rows_out (int32 [1]) receives the rows this rank gets."""
         _native.check(self.lib.lp_ep_exchange(counts.data_ptr(), self.peer_ctl.data_ptr(), self.world, self.el,
                                               self.rank, self.dest_base.data_ptr(), self.off_local.data_ptr(),
-                                              stream), "lp_ep_exchange")
+                                              rows_out.data_ptr() if rows_out is not None else None, stream),
+                      "lp_ep_exchange")
 
     def close(self) -> None:
         """Collective: every rank must call it (peers may still read this region until all have synced)."""
@@ -373,7 +374,7 @@ class PeerEP:
                                          self._offsets.data_ptr(), self._slot_of.data_ptr(), self._tok_of.data_ptr(),
                                          None, ws.data_ptr(), ws.numel(), st), f"lp_moe_permute (T={T})")
         mark(1)
-        rg.exchange(counts, st)  # counts to every rank + wait for every source + plan (one launch)
+        rg.exchange(counts, st, self._recv_rows)  # counts to every rank + wait for every source + plan
         _native.check(lib.lp_ep_dispatch(x.data_ptr(), self._ids.data_ptr(), self._slot_of.data_ptr(),
                                          self._offsets.data_ptr(), rg.dest_base.data_ptr(), rg.peer_recv.data_ptr(),
                                          T, H, k, el, self._dest_rank.data_ptr(), self._dest_row.data_ptr(), st),
@@ -387,7 +388,6 @@ class PeerEP:
                                               self.w13.data_ptr(), self.w2.data_ptr(), H, s.ffn, el,
                                               act.data_ptr(), rg.y_out_ptr, ws.data_ptr(), ws.numel(), st),
                       "lp_moe_experts_rows")
-        self._recv_rows.copy_(rg.off_local[el:el + 1])  # the region's off_local is rewritten by the next layer
         rg.barrier(st)
         mark(3)
         y = out if out is not None else torch.empty((T, H), dtype=torch.bfloat16, device=self.device)
@@ -396,7 +396,8 @@ class PeerEP:
         # no end-of-layer barrier: see ep_p2p.cuh (the next exchange / dispatch barrier orders reuse)
         mark(4)
         self.last_ids, self.last_weights = ids, w
-        return y, EPStats(counts, self._recv_rows[0], counts.view(P, el).sum(1), [], s)
+        # (send_splits: rows per destination = counts.view(P, El).sum(1), left to the caller: no extra launch)
+        return y, EPStats(counts, self._recv_rows[0], None, [], s)
 
     __call__ = forward
 
