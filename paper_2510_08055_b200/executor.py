@@ -180,6 +180,33 @@ def _timed(events):
     return e0, e1
 
 
+def shard_rows(T: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank `rank`'s contiguous share [lo, hi) of a segment's T rows (token-level data parallelism)."""
+    return T * rank // world, T * (rank + 1) // world
+
+
+def gather_rows(x: torch.Tensor, xl: torch.Tensor, rank: int, world: int, group=None,
+                via_host: bool = False) -> torch.Tensor:
+    """All-gather every rank's processed share back into the replicated x (in place; uneven shares
+    padded to ceil(T / world) rows). via_host: stage through host memory (gloo; ranks sharing a GPU)."""
+    T, H = x.shape
+    n = (T + world - 1) // world
+    pad = torch.zeros((n, H), dtype=x.dtype, device=x.device)
+    pad[: xl.shape[0]].copy_(xl)
+    if via_host:
+        parts = [torch.empty((n, H), dtype=x.dtype) for _ in range(world)]
+        dist.all_gather(parts, pad.cpu(), group=group)
+        full = torch.cat(parts).to(x.device)
+    else:
+        full = torch.empty((world * n, H), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(full, pad, group=group)
+    for r in range(world):
+        a, b = shard_rows(T, r, world)
+        if r != rank and b > a:
+            x[a:b].copy_(full[r * n: r * n + (b - a)])
+    return x
+
+
 class EPMoEModel:
     """`num_layers` expert-parallel MoE layers (BASELINE config 5): rank r of P holds
     experts [r*E/P, (r+1)*E/P) of every layer (ep.PeerEP: fused dispatch / combine over peer
@@ -214,7 +241,7 @@ class EPMoEModel:
         self._gloo = dist.get_backend(group) != "nccl"
 
     def _rows(self, T: int) -> tuple[int, int]:
-        return T * self.rank // self.world, T * (self.rank + 1) // self.world
+        return shard_rows(T, self.rank, self.world)
 
     def run_segment(self, x: torch.Tensor, l0: int, l1: int, counts: torch.Tensor, events=None) -> torch.Tensor:
         T, H = x.shape
@@ -236,24 +263,7 @@ class EPMoEModel:
         return self._gather(x, xl)
 
     def _gather(self, x: torch.Tensor, xl: torch.Tensor) -> torch.Tensor:
-        """Every rank's processed rows back into the replicated x (uneven shares padded)."""
-        T, H = x.shape
-        P = self.world
-        n = (T + P - 1) // P
-        pad = torch.zeros((n, H), dtype=x.dtype, device=x.device)
-        pad[: xl.shape[0]].copy_(xl)
-        if self._gloo:  # protocol tests: ranks share one GPU, collectives staged through the host
-            parts = [torch.empty((n, H), dtype=x.dtype) for _ in range(P)]
-            dist.all_gather(parts, pad.cpu(), group=self.group)
-            full = torch.cat(parts).to(x.device)
-        else:
-            full = torch.empty((P * n, H), dtype=x.dtype, device=x.device)
-            dist.all_gather_into_tensor(full, pad, group=self.group)
-        for r in range(P):
-            a, b = T * r // P, T * (r + 1) // P
-            if r != self.rank and b > a:
-                x[a:b].copy_(full[r * n: r * n + (b - a)])
-        return x
+        return gather_rows(x, xl, self.rank, self.world, self.group, via_host=self._gloo)
 
     def _reduce(self, t: torch.Tensor, op) -> torch.Tensor:
         if self._gloo:
