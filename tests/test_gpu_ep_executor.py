@@ -27,14 +27,25 @@ def _free_port():
     return p
 
 
-def _engine_run(stack, policy, lens, out):
+def _model(ms, shape_name):
+    if shape_name == "tiny":
+        return ms.types.ModelSpec(name="tiny-moe", num_layers=4, num_experts=16, top_k=2, bytes_per_expert=196608,
+                                  dense_bytes_per_layer=524288, flops_per_token_per_expert=196608,
+                                  attn_flops_per_token_per_ctx=4096, kv_bytes_per_token=4096, hidden_dim=256)
+    import dataclasses
+
+    from paper_2510_08055_b200 import refdrive
+    from paper_2510_08055_b200.types import QWEN3_30B_A3B_MODEL
+
+    return dataclasses.replace(refdrive.reference_model(QWEN3_30B_A3B_MODEL), num_layers=4)  # 4-layer Qwen stack
+
+
+def _engine_run(stack, policy, lens, out, shape_name="tiny"):
     from paper_2510_08055_b200 import refdrive
     from paper_2510_08055_b200.executor import LayeredExecutor
 
     ms = refdrive.import_moesim()
-    model = ms.types.ModelSpec(name="tiny-moe", num_layers=4, num_experts=16, top_k=2, bytes_per_expert=196608,
-                               dense_bytes_per_layer=524288, flops_per_token_per_expert=196608,
-                               attn_flops_per_token_per_ctx=4096, kv_bytes_per_token=4096, hidden_dim=256)
+    model = _model(ms, shape_name)
     cfg = ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=512, group_token_target=512)
     reqs = [ms.types.Request(id=i, arrival_s=0.0, input_len=n, output_len=out) for i, n in enumerate(lens)]
     ex = LayeredExecutor(stack, keep_final_prompt=True)
@@ -43,7 +54,7 @@ def _engine_run(stack, policy, lens, out):
     return res, ex
 
 
-def _worker(rank, world, port, policy, lens, out, q):
+def _worker(rank, world, port, policy, lens, out, q, shape_name="tiny"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -51,14 +62,15 @@ def _worker(rank, world, port, policy, lens, out, q):
         import torch.distributed as dist
 
         from paper_2510_08055_b200.executor import EPMoEModel, MoEModel
-        from paper_2510_08055_b200.types import TINY
+        from paper_2510_08055_b200.types import QWEN3_30B_A3B, TINY
 
+        shape = TINY if shape_name == "tiny" else QWEN3_30B_A3B
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-        ep = EPMoEModel(TINY, 4, rank, world, max_tokens=4096, device=dev, seed=3)
-        res, ex = _engine_run(ep, policy, lens, out)
-        ref_res, ref_ex = _engine_run(MoEModel(TINY, 4, device=dev, seed=3), policy, lens, out)
+        ep = EPMoEModel(shape, 4, rank, world, max_tokens=4096, device=dev, seed=3)
+        res, ex = _engine_run(ep, policy, lens, out, shape_name)
+        ref_res, ref_ex = _engine_run(MoEModel(shape, 4, device=dev, seed=3), policy, lens, out, shape_name)
         torch.cuda.synchronize()
         ok, msg = True, ""
         for rid in range(len(lens)):
@@ -81,7 +93,7 @@ def _worker(rank, world, port, policy, lens, out, q):
         q.put((rank, False, traceback.format_exc()[-3000:]))
 
 
-def _run(policy, lens, out=3, world=2):
+def _run(policy, lens, out=3, world=2, shape_name="tiny"):
     import queue
 
     import torch.multiprocessing as mp
@@ -89,7 +101,8 @@ def _run(policy, lens, out=3, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, policy, lens, out, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, policy, lens, out, q, shape_name))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -127,3 +140,13 @@ def test_ep_stack_chunked_matches_single_gpu(cuda):
     if not refdrive.reference_available():
         pytest.skip("the reference (moesim) is not importable: tools/vendor_reference.sh")
     _run("chunked", (900, 77))
+
+
+def test_ep_stack_qwen_layered_matches_single_gpu(cuda):
+    """Qwen3-30B-A3B-shaped 4-layer stack (64 experts per rank): layered prefill of two prompts with
+    decodes riding along, EP ≡ single GPU bit for bit."""
+    from paper_2510_08055_b200 import refdrive
+
+    if not refdrive.reference_available():
+        pytest.skip("the reference (moesim) is not importable: tools/vendor_reference.sh")
+    _run("layered", (700, 300), out=2, shape_name="qwen")

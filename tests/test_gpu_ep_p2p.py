@@ -47,7 +47,10 @@ def _worker(rank, world, port, shape_name, tokens, skew, layers, q, physical=Fal
         dev = torch.device("cuda", rank if physical else 0)
         torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-        s = {"tiny": TINY, "qwen": QWEN3_30B_A3B, "e256": MoEShape(512, 256, 256, 8, False)}[shape_name]
+        from paper_2510_08055_b200 import GPT_OSS_20B
+
+        s = {"tiny": TINY, "qwen": QWEN3_30B_A3B, "e256": MoEShape(512, 256, 256, 8, False),
+             "gptoss": GPT_OSS_20B}[shape_name]
         wr = router_weight(s.num_experts, s.hidden, 21).float()
         if skew:  # every token of every rank prefers the experts of rank 0
             wr[: s.top_k, s.hidden - 1] = 16.0
@@ -151,6 +154,11 @@ def test_peer_ep2_graph_captured_layers(cuda):
 
 def test_peer_ep2_skewed_to_rank0_and_empty_rank(cuda):
     _run("tiny", [80, 0], skew=True)
+
+
+def test_peer_ep2_gpt_oss_shape(cuda):
+    """The reference's second model config (H = I = 2880: not multiples of 128; 32 experts top-4)."""
+    _run("gptoss", [300, 45])
 
 
 def test_peer_ep2_large_uneven_batches_max_experts(cuda):
