@@ -294,18 +294,130 @@ class MoEIteration:
     device_s: float            # device time of the MoE layer calls (CUDA events around the segments)
     routed: list               # routed tokens through each layer (engine.py:137-154 semantics)
     experts_hit: list          # experts the routing touched in each layer (nnz of the real counts)
+    includes_attention: bool = False  # device_s also covers attention + dense projections (measured)
 
 
 def _finished(r) -> bool:
     return getattr(r.phase, "value", r.phase) == "finished"
 
 
+class AttentionDense:
+    """Measured attention + dense projections for the serving executor: per layer,
+    RMSNorm → QKV projection (cuBLAS) → causal GQA attention over each request's KV cache (PyTorch
+    scaled_dot_product_attention, library kernels) → output projection (cuBLAS) → residual add.
+
+    Qwen3-30B-A3B attention shapes (configs/qwen30b.toml): 32 query heads, 4 KV heads, head_dim 128
+    (Wqkv [4096 + 2 x 512, 2048], Wo [2048, 4096], random init; no RoPE — positions only enter
+    through the causal masks). Each request owns a KV cache [layers, input_len + output_len, 4, 128]
+    (K and V, bf16), filled by its prefill slices (layered: the whole prompt per layer group;
+    chunked: the chunk attends to the cached KV of the earlier chunks) and one row per decode step;
+    decode rows at the same context length are batched into one SDPA call. These are library
+    kernels on the serving path, not the MoE hot path: they replace the reference's modelled
+    attention_cost / dense_cost (costmodel.py:88-145) with measured time."""
+
+    HEADS, KV_HEADS, HEAD_DIM = 32, 4, 128
+
+    def __init__(self, hidden: int, num_layers: int, device, seed: int = 0, std: float = 0.02):
+        self.H, self.L = hidden, num_layers
+        self.device = torch.device(device)
+        qd, kd = self.HEADS * self.HEAD_DIM, self.KV_HEADS * self.HEAD_DIM
+        self.qd, self.kd = qd, kd
+        g = torch.Generator(device=self.device).manual_seed(seed * 7919 + 17)
+        self.wqkv = [(torch.randn((qd + 2 * kd, hidden), generator=g, device=self.device) * std).to(torch.bfloat16)
+                     for _ in range(num_layers)]
+        self.wo = [(torch.randn((hidden, qd), generator=g, device=self.device) * std).to(torch.bfloat16)
+                   for _ in range(num_layers)]
+        self.kv: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+
+    def cache(self, rid: int, length: int):
+        c = self.kv.get(rid)
+        if c is None:
+            shape = (self.L, length, self.KV_HEADS, self.HEAD_DIM)
+            c = (torch.empty(shape, dtype=torch.bfloat16, device=self.device),
+                 torch.empty(shape, dtype=torch.bfloat16, device=self.device))
+            self.kv[rid] = c
+        return c
+
+    def drop(self, rid: int) -> None:
+        self.kv.pop(rid, None)
+
+    def _heads(self, t: torch.Tensor) -> torch.Tensor:
+        """[B, 4, ctx, 128] KV heads -> [B, 32, ctx, 128] (GQA by repetition: SDPA's fused backends then
+        take the lower-right causal bias; with enable_gqa some shapes fell back to the math path)."""
+        return t.repeat_interleave(self.HEADS // self.KV_HEADS, dim=1)
+
+    def layer(self, l: int, h: torch.Tensor, spans: list) -> None:
+        """h [T, H] (in place) += Wo · attention(QKV(RMSNorm(h))); spans: (rid, pos0, n, cache_len) per
+        consecutive row run, decode rows first (n = 1), in row order."""
+        import torch.nn.functional as F
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        T = h.shape[0]
+        # cuDNN's sm100 attention first (PyTorch's own flash kernel, built for sm80/90, ran the
+        # lower-right-causal chunk case ~5x slower on B200)
+        order = [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION,
+                 SDPBackend.MATH]
+        with sdpa_kernel(order, set_priority=True):
+            self._layer(F, l, h, T, spans)
+
+    def _layer(self, F, l: int, h: torch.Tensor, T: int, spans: list) -> None:
+        xn = torch.empty_like(h)
+        add_rmsnorm(h, None, xn)
+        qkv = xn @ self.wqkv[l].t()
+        q = qkv[:, :self.qd].view(T, self.HEADS, self.HEAD_DIM)
+        k = qkv[:, self.qd:self.qd + self.kd].view(T, self.KV_HEADS, self.HEAD_DIM)
+        v = qkv[:, self.qd + self.kd:].view(T, self.KV_HEADS, self.HEAD_DIM)
+        out = torch.empty((T, self.HEADS, self.HEAD_DIM), dtype=h.dtype, device=h.device)
+        row = 0
+        i = 0
+        while i < len(spans):
+            rid, pos0, n, clen = spans[i]
+            if n == 1:  # a run of decode rows at the same position: one batched SDPA
+                j = i
+                while j < len(spans) and spans[j][2] == 1 and spans[j][1] == pos0:
+                    j += 1
+                ks, vs = [], []
+                for b in range(i, j):
+                    K, V = self.cache(spans[b][0], spans[b][3])
+                    K[l, pos0] = k[row + b - i]
+                    V[l, pos0] = v[row + b - i]
+                    ks.append(K[l, :pos0 + 1])
+                    vs.append(V[l, :pos0 + 1])
+                B = j - i
+                qb = q[row:row + B].unsqueeze(2).contiguous()                      # [B, 32, 1, 128]
+                kb = self._heads(torch.stack(ks).transpose(1, 2))                  # [B, 32, ctx, 128]
+                vb = self._heads(torch.stack(vs).transpose(1, 2))
+                out[row:row + B] = F.scaled_dot_product_attention(qb, kb, vb)[:, :, 0]
+                row += B
+                i = j
+                continue
+            K, V = self.cache(rid, clen)
+            K[l, pos0:pos0 + n] = k[row:row + n]
+            V[l, pos0:pos0 + n] = v[row:row + n]
+            qb = q[row:row + n].transpose(0, 1).unsqueeze(0).contiguous()          # [1, 32, n, 128]
+            kb = self._heads(K[l, :pos0 + n].transpose(0, 1).unsqueeze(0))          # [1, 32, pos0 + n, 128]
+            vb = self._heads(V[l, :pos0 + n].transpose(0, 1).unsqueeze(0))
+            if pos0 == 0:
+                o = F.scaled_dot_product_attention(qb, kb, vb, is_causal=True)
+            else:  # a later chunk: query i (position pos0 + i) sees keys 0 .. pos0 + i (lower-right causal,
+                # which SDPA's fused kernels take directly; an explicit mask falls back to the math path)
+                from torch.nn.attention.bias import causal_lower_right
+
+                o = F.scaled_dot_product_attention(qb, kb, vb, attn_mask=causal_lower_right(n, pos0 + n))
+            out[row:row + n] = o[0].transpose(0, 1)
+            row += n
+            i += 1
+        h += out.view(T, self.qd) @ self.wo[l].t()
+
+
 class LayeredExecutor:
     """Runs a reference `BatchPlan` on the resident layer stack (duck-typed on moesim's SimState:
     `state.request(rid)` with `input_len` and `phase`)."""
 
-    def __init__(self, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False):
+    def __init__(self, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False,
+                 attention: AttentionDense | None = None):
         self.stack = stack
+        self.attention = attention  # measured attention + dense projections (None: modelled by the reference)
         self.keep_final_prompt = keep_final_prompt
         self.final_prompt: dict[int, torch.Tensor] = {}
         self.final_decode: dict[int, torch.Tensor] = {}  # last decode hidden row of finished requests
@@ -339,6 +451,9 @@ class LayeredExecutor:
 
     def run_plan(self, state, plan) -> MoEIteration:
         L = self.stack.num_layers
+        if self.attention is not None:  # KV caches of requests the engine retired since the last call
+            for rid in [k for k in self.attention.kv if _finished(state.request(k))]:
+                self.attention.drop(rid)
         for rid in [k for k in self.stash if _finished(state.request(k))]:
             h = self.stash.pop(rid)  # prompt finished without a decode step (output_len == 1)
             if self.keep_final_prompt:
@@ -352,7 +467,7 @@ class LayeredExecutor:
         for a in plan.prefill_assignments:
             for layer in range(a.layer_start, a.layer_end):
                 routed[layer] += a.num_tokens
-        events = []
+        events, attn_events = [], []
         dec = torch.stack(dec_rows) if D else torch.empty((0, self.H), dtype=torch.bfloat16, device=self.dev)
         for l0, l1 in zip(cuts, cuts[1:]):
             act = [a for a in plan.prefill_assignments if a.layer_start <= l0 < a.layer_end]
@@ -360,9 +475,27 @@ class LayeredExecutor:
             if sum(p.shape[0] for p in parts) == 0:
                 continue
             x = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
-            # only the MoE work is timed (not the embedding, the concatenation, the copy-back or an
-            # expert-parallel stack's row gather): the stack records the events
-            x = self.stack.run_segment(x, l0, l1, counts, events)
+            if self.attention is None:
+                # only the MoE work is timed (not the embedding, the concatenation, the copy-back or an
+                # expert-parallel stack's row gather): the stack records the events
+                x = self.stack.run_segment(x, l0, l1, counts, events)
+            else:  # per layer: attention + dense (measured), then the MoE sublayer
+                spans = [(rid, state.request(rid).input_len + state.request(rid).tokens_emitted - 1, 1,
+                          state.request(rid).input_len + state.request(rid).output_len) for rid in plan.decode_ids]
+                spans += [(a.request_id, a.token_start, a.num_tokens,
+                           state.request(a.request_id).input_len + state.request(a.request_id).output_len)
+                          for a in act]
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for layer in range(l0, l1):
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record()
+                    self.attention.layer(layer, x, spans)
+                    a1.record()
+                    attn_events.append((a0, a1))
+                    x = self.stack.run_segment(x, layer, layer + 1, counts)
+                e1.record()
+                events.append((e0, e1))
             dec = x[:D]
             off = D
             for a in act:
@@ -375,11 +508,12 @@ class LayeredExecutor:
         moe_s = self.stack.reduce_max(sum(a.elapsed_time(b) for a, b in events) * 1e-3)
         nnz = (self.stack.reduce_counts(counts) > 0).sum(dim=1).cpu().tolist()
         self.iter_log.append({"moe_s": moe_s, "routed": routed, "experts_hit": nnz, "decode": D,
-                              "prefill_tokens": plan.prefill_tokens})
+                              "prefill_tokens": plan.prefill_tokens,
+                              "attn_s": sum(a.elapsed_time(b) for a, b in attn_events) * 1e-3})
         # drop finished requests' state (the engine retires them after this call)
         live = set(plan.decode_ids) | {r.id for r in state.decoding}
         for rid in [k for k in self.decode_row if k not in live]:
             row = self.decode_row.pop(rid)
             if self.keep_final_prompt:
                 self.final_decode[rid] = row
-        return MoEIteration(moe_s, routed, nnz)
+        return MoEIteration(moe_s, routed, nnz, self.attention is not None)

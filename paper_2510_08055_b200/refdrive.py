@@ -142,7 +142,16 @@ def measured_costs(coverage=None, executor=None):
         kernels, decode_ctx = base_iter(state, plan, coverage_model)
         it = executor.run_plan(state, plan)
         moe = measured_moe_kernel(state.model, it.routed, it.experts_hit, it.device_s)
-        return [moe] + [k for k in kernels if k.kind != cmod.KernelKind.MOE_FFN], decode_ctx
+        rest = [k for k in kernels if k.kind != cmod.KernelKind.MOE_FFN]
+        if getattr(it, "includes_attention", False):
+            # attention + dense projections ran on the GPU and are inside device_s: keep their
+            # modelled flops / bytes (energy, reporting) but charge no modelled time for them
+            measured = (cmod.KernelKind.DENSE_PROJ, cmod.KernelKind.ATTENTION_PREFILL,
+                        cmod.KernelKind.ATTENTION_DECODE)
+            rest = [MK(kind=k.kind, flops=k.flops, hbm_bytes=k.hbm_bytes,
+                       expert_weight_bytes=k.expert_weight_bytes, measured_s=0.0) if k.kind in measured else k
+                    for k in rest]
+        return [moe] + rest, decode_ctx
 
     eng.iteration_runtime = iteration_runtime
     cli.kernel_runtime = kernel_runtime

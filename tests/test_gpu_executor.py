@@ -155,3 +155,60 @@ def test_reference_chunk_bench_with_measured_coverage(qwen_layer):
         assert r["moe_runtime_s"] > 0 and r["moe_runtime_s"] != m["moe_runtime_s"]
     # one 4096-token chunk streams the weights once per layer instead of 8 times
     assert rows[1]["moe_expert_bytes"] * 8 == rows[0]["moe_expert_bytes"]
+
+
+def _attn_reference(att, l, xs):
+    """fp32 restatement of AttentionDense.layer over a whole prompt: RMSNorm (unit gain), QKV,
+    causal GQA attention, output projection, residual."""
+    x = xs.float()
+    xn = x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6)
+    qkv = xn @ att.wqkv[l].float().t()
+    T = x.shape[0]
+    q = qkv[:, :att.qd].view(T, 32, 128).transpose(0, 1)
+    k = qkv[:, att.qd:att.qd + att.kd].view(T, 4, 128).transpose(0, 1).repeat_interleave(8, 0)
+    v = qkv[:, att.qd + att.kd:].view(T, 4, 128).transpose(0, 1).repeat_interleave(8, 0)
+    s = (q @ k.transpose(1, 2)) / 128 ** 0.5
+    s = s.masked_fill(torch.triu(torch.ones(T, T, dtype=torch.bool, device=x.device), 1), float("-inf"))
+    o = torch.softmax(s, -1) @ v
+    return x + o.transpose(0, 1).reshape(T, att.qd) @ att.wo[l].float().t()
+
+
+def test_attention_dense_chunks_and_decode_match_fp32(cuda):
+    """AttentionDense: a prompt prefilled in two chunks (the second attends to the cached first) and
+    then one decode row give the rows a single fp32 causal pass over the whole sequence gives."""
+    from paper_2510_08055_b200.executor import AttentionDense
+
+    att = AttentionDense(256, 2, cuda, seed=5)
+    g = torch.Generator(device=cuda).manual_seed(3)
+    xs = torch.randn((20, 256), generator=g, device=cuda).to(torch.bfloat16)
+    ref = _attn_reference(att, 1, xs)
+    a = xs[:12].clone()
+    att.layer(1, a, [(7, 0, 12, 20)])          # chunk 1: positions 0..11
+    b = xs[12:19].clone()
+    att.layer(1, b, [(7, 12, 7, 20)])          # chunk 2: positions 12..18 over the cached 0..11
+    d = xs[19:20].clone()
+    att.layer(1, d, [(7, 19, 1, 20)])          # decode row at position 19
+    got = torch.cat([a, b, d]).float()
+    err = ((got - ref).norm() / ref.norm()).item()
+    assert err < 1e-2, err
+
+
+def test_layered_vs_chunked_with_measured_attention(stack):
+    """With measured attention + dense projections the reference engine's layered and chunked runs
+    reach the same final prompt hidden states (bf16: different chunking gives different rounding,
+    so a tolerance), and the engine charges the measured time for attention too."""
+    from paper_2510_08055_b200.executor import AttentionDense
+
+    reqs = _reqs((1024, 300), 3)
+    out = {}
+    for policy in ("layered", "chunked"):
+        att = AttentionDense(TINY.hidden, 4, stack.device, seed=9)
+        ex = LayeredExecutor(stack, keep_final_prompt=True, attention=att)
+        with refdrive.measured_costs(executor=ex):
+            res = ms.engine.run(TINY_MODEL, refdrive.b200_hardware(), _cfg(policy), reqs, _table())
+        assert all(it["moe_s"] > 0 for it in ex.iter_log)
+        assert len(att.kv) <= len(reqs)  # retired requests' caches are released on the next call
+        out[policy] = ex
+    for rid in range(2):
+        a, b = out["layered"].final_prompt[rid].float(), out["chunked"].final_prompt[rid].float()
+        assert ((a - b).norm() / a.norm()).item() < 3e-2, rid

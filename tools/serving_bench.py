@@ -48,11 +48,15 @@ def _h100():
     return ms.config.load_run_config(refdrive.reference_config("qwen_arxiv_layered.toml")).hardware
 
 
+ATTENTION = False  # --attention: measured attention + dense projections (executor.AttentionDense)
+
+
 def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, graphs=0):
-    from paper_2510_08055_b200.executor import LayeredExecutor
+    from paper_2510_08055_b200.executor import AttentionDense, LayeredExecutor
 
     cfg = ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=chunk, group_token_target=target)
-    ex = LayeredExecutor(stack)
+    att = AttentionDense(QWEN3_30B_A3B.hidden, MODEL.num_layers, stack.device, seed=11) if ATTENTION else None
+    ex = LayeredExecutor(stack, attention=att)
     t0 = time.time()
     with refdrive.measured_costs(executor=ex):
         res = ms.engine.run(MODEL, refdrive.b200_hardware(), cfg, reqs, ms.coverage.EmpiricalTable())
@@ -63,7 +67,9 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
            "expert_load_GB": s["total_expert_load_bytes"] / 1e9, "moe_time_ms": moe_s * 1e3,
            "moe_us_per_layer_call": 1e6 * moe_s / max(1, sum(sum(1 for n in it["routed"] if n)
                                                              for it in ex.iter_log)),
-           "decode_graph_tokens": graphs, "wall_s": wall}
+           "decode_graph_tokens": graphs, "wall_s": wall,
+           "measured": "MoE + attention + dense projections (attention: PyTorch SDPA, dense: cuBLAS)" if ATTENTION
+           else "MoE (attention / dense projections: the reference's roofline model on B200 peaks)"}
     if focus is not None:
         r = next(r for r in res.requests if r.id == focus)
         out["focus_ttft_s"] = r.first_token_s - r.arrival_s
@@ -81,6 +87,8 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
     out["reference_model_h100"] = {k: m[k] for k in ("ttft_mean_s", "tbt_mean_s", "total_expert_load_bytes",
                                                      "num_iterations")}
     out["gpus"] = getattr(stack, "world", 1)
+    if ATTENTION:
+        out["attention_dense_ms"] = 1e3 * sum(it["attn_s"] for it in ex.iter_log)
     if emit and EMIT:
         print(json.dumps(out), flush=True)
     return out
@@ -100,6 +108,8 @@ def main():
     ap.add_argument("--trace", default=None, help="c5: a reference trace CSV (moesim workload.export_trace) "
                                                  "instead of the config's generated workload")
     ap.add_argument("--gpus", type=int, default=1, help="expert-parallel ranks (one per GPU)")
+    ap.add_argument("--attention", action="store_true",
+                    help="measure attention + dense projections too (library kernels; single GPU)")
     ap.add_argument("--max-tokens", type=int, default=40960,
                     help="--gpus > 1: the largest segment (rows of one layer call, all ranks) to size EP buffers")
     a = ap.parse_args()
@@ -115,6 +125,10 @@ def main():
                                   os.path.abspath(__file__), *sys.argv[1:]]))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    global ATTENTION
+    ATTENTION = a.attention
+    if ATTENTION and world > 1:
+        raise SystemExit("serving_bench.py: --attention is a single-GPU mode")
     if world != a.gpus:
         raise SystemExit(f"serving_bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
 
@@ -157,9 +171,13 @@ def main():
         reqs = [R(id=0, arrival_s=0.0, input_len=L, output_len=1)]
         run_one(stack, "warmup", "chunked", 8192, 512, reqs, focus=0, emit=False)
         for chunk in (512, 1024, 2048, 4096, 8192):
+            if ATTENTION:  # untimed pass first: cuDNN builds an attention plan per new (chunk, context) shape
+                run_one(stack, "warmup", "chunked", chunk, 512, reqs, focus=0, emit=False)
             run_one(stack, f"c4_chunked_c{chunk}", "chunked", chunk, 512, reqs, focus=0, graphs=g)
         for groups in (1, 2, 3, 4, 6, 8, 12, 16, 24, 48):
             target = math.ceil(L / groups)
+            if ATTENTION:
+                run_one(stack, "warmup", "layered", 512, target, reqs, focus=0, emit=False)
             run_one(stack, f"c4_layered_G{groups}", "layered", 512, target, reqs, focus=0, graphs=g)
     else:
         if a.trace:
