@@ -16,3 +16,8 @@ LP_T=576 LP_ITERS=6 timeout 600 ncu --set full --clock-control none --import-sou
 LP_T=8224 LP_ITERS=4 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_experts -s 2 -c 1 -o $O/k_experts_8224 python tools/prof_layer.py >> $O/ncu_full.log 2>&1
 LP_TINY_ITEMS=1 LP_T=1 timeout 120 python tools/trace_layer.py > $O/trace_decode_T1.txt 2>&1
 LP_T=576 timeout 120 python tools/trace_layer.py > $O/trace_T576.txt 2>&1
+timeout 600 python tools/ep_overhead.py 1 64 576 2048 > $O/ep_overhead_world1.jsonl 2>$O/ep_overhead.err
+timeout 1500 python tools/serving_bench.py --config c3 > $O/serving_c3.jsonl 2>$O/serving_c3.err
+timeout 1500 python tools/serving_bench.py --config c4 > $O/serving_c4.jsonl 2>$O/serving_c4.err
+timeout 2400 python tools/serving_bench.py --config c5 --requests 100 > $O/serving_c5.jsonl 2>$O/serving_c5.err
+timeout 2000 python tools/serving_bench.py --config c4 --attention > $O/serving_c4_attention.jsonl 2>$O/serving_c4_attention.err
