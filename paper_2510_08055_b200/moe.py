@@ -47,10 +47,17 @@ class MoEStats:
 
 
 def _stream_ptr(device: torch.device) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+    # the raw current-stream handle (torch.cuda.current_stream() builds a Stream object per call:
+    # a few us of host time on every decode-size layer call)
+    return torch._C._cuda_getCurrentRawStream(device.index if device.index is not None else
+                                              torch.cuda.current_device())
 
 
 def _check_tensor(name: str, t: torch.Tensor, shape: tuple, dtype: torch.dtype) -> None:
+    # one cheap combined test on the hot path; the messages are only formatted on failure
+    if (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.shape == shape
+            and t.is_contiguous()):
+        return
     require(isinstance(t, torch.Tensor), f"{name} must be a torch.Tensor")
     require(t.is_cuda, f"{name} must be a CUDA tensor (no CPU path exists), got device {t.device}")
     require(t.dtype == dtype, f"{name} must be {dtype}, got {t.dtype}")
@@ -96,11 +103,17 @@ class GpuMoE:
         self._ws = workspace if workspace is not None else Workspace(self.device)
         self._route_cap = 0
         self._route_bufs: tuple[torch.Tensor, torch.Tensor, torch.Tensor] | None = None
+        self._ws_bytes: dict[int, int] = {}   # workspace bytes per T (one ctypes call per new T)
+        self._wptrs = (wr.data_ptr(), w13.data_ptr(), w2.data_ptr())
 
     # ------------------------------------------------------------ workspace
     def workspace_bytes(self, T: int) -> int:
-        s = self.shape
-        return int(self._lib.lp_moe_workspace_bytes(T, s.hidden, s.ffn, s.num_experts, s.top_k))
+        n = self._ws_bytes.get(T)
+        if n is None:
+            s = self.shape
+            n = int(self._lib.lp_moe_workspace_bytes(T, s.hidden, s.ffn, s.num_experts, s.top_k))
+            self._ws_bytes[T] = n
+        return n
 
     def workspace(self, T: int) -> torch.Tensor:
         # zero-filled on (re)allocation: the header holds self-resetting scheduler words (lpmoe.h)
@@ -127,7 +140,7 @@ class GpuMoE:
         the layer's internal per-T buffer (the executor keeps one row per layer).
         """
         s = self.shape
-        require(x.dim() == 2, f"x must be 2-D [T, H], got {tuple(x.shape)}")
+        require(x.dim() == 2, "x must be 2-D [T, H]")
         T = x.shape[0]
         _check_tensor("x", x, (T, s.hidden), torch.bfloat16)
         y = torch.empty_like(x) if out is None else out
@@ -137,12 +150,14 @@ class GpuMoE:
             _check_tensor("counts_out", counts_out, (s.num_experts,), torch.int32)
             counts = counts_out
         ws = self.workspace(T)
+        wr, w13, w2 = self._wptrs
         rc = self._lib.lp_moe_forward(
-            x.data_ptr(), self.wr.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+            x.data_ptr(), wr, w13, w2,
             T, s.hidden, s.ffn, s.num_experts, s.top_k, int(s.norm_topk_prob),
             y.data_ptr(), ids.data_ptr(), w.data_ptr(), counts.data_ptr(),
             ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
-        _native.check(rc, "lp_moe_forward")
+        if rc:
+            _native.check(rc, "lp_moe_forward")
         self.last_ids, self.last_weights = ids, w
         return y, MoEStats(counts, s)
 
