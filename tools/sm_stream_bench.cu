@@ -49,10 +49,15 @@ __global__ void __launch_bounds__(64, 1) k_sm_stream(const __grid_constant__ CUt
       mbar_arrive_expect_tx(&full[stage], kStage);
       if (boxes == 1) {
         tma_load_2d(smem + stage * kStage, &tm, &full[stage], kb * 64, static_cast<int>(row_base + slab * 128), pol);
-      } else {  // gate/up-like: two 64-row boxes 768 rows apart
+      } else if (boxes == 2) {  // gate/up-like: two 64-row boxes 768 rows apart
         tma_load_2d(smem + stage * kStage, &tm, &full[stage], kb * 64, static_cast<int>(row_base + slab * 128), pol);
         tma_load_2d(smem + stage * kStage + 8192, &tm, &full[stage], kb * 64,
                     static_cast<int>(row_base + slab * 128 + 768), pol);
+      } else {  // the same 128 rows as `boxes == 1`, in `-boxes` boxes of 128/-boxes rows (no overlap)
+        const int nb = -boxes, rows = 128 / nb;
+        for (int b = 0; b < nb; ++b)
+          tma_load_2d(smem + stage * kStage + b * rows * 128, &tm, &full[stage], kb * 64,
+                      static_cast<int>(row_base + slab * 128 + b * rows), pol);
       }
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
@@ -118,6 +123,21 @@ int main() {
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0) {
     printf("encode failed\n"); return 1;
   }
+  // box-count sensitivity: the same 128-row x 16 KiB stages as 1, 2, 4 boxes (non-overlapping rows)
+  CUtensorMap tm32, tm16;
+  cuuint32_t box32[2] = {64, 32}, box16b[2] = {64, 64};
+  if (enc(&tm32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box32, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0 ||
+      enc(&tm16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box16b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0) {
+    printf("encode failed\n"); return 1;
+  }
+  for (int ctas : {96, 148}) {
+    run<11>(tm, ctas, 32, 0, 1, "1x128");
+    run<11>(tm16, ctas, 32, 0, -2, "2x64nov");
+    run<11>(tm32, ctas, 32, 0, -4, "4x32nov");
+  }
+  if (getenv("BOXES_ONLY")) return 0;
   // hot L2 reads (router weight pattern): every CTA streams the same 256 KB / 128 KB
   run<11>(tm, 148, 16, 1, 1, "hot");
   run<11>(tm, 148, 8, 1, 1, "hot");
