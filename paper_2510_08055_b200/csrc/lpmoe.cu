@@ -754,6 +754,8 @@ int launch_experts(const void* src, int src_rows, const int32_t* tok_of, int S, 
 // Tile schedule from externally supplied offsets (staged / expert-parallel use).
 __global__ void k_plan(const int32_t* __restrict__ offsets, int E, int max_n, int32_t* __restrict__ tile_prefix,
                        int32_t* __restrict__ tile_rows, uint32_t* __restrict__ sched) {
+  lp::pdl_trigger();  // PDL: the expert kernel's prologue (TMEM, barriers, L2 weight prefetch) overlaps
+  lp::pdl_wait();
   extern __shared__ int32_t s_til[];
   const int e = threadIdx.x;
   const int n = (e < E) ? offsets[e + 1] - offsets[e] : 0;
@@ -869,9 +871,7 @@ int lp_moe_experts_rows(const void* x_perm, const int32_t* offsets, int S, int S
   uint32_t* sched = at<uint32_t>(ws, kSchedOff);
   const int max_n = pick_max_n(S_hint > 0 ? S_hint : S, E);
   const int sb = (E + 31) / 32 * 32;
-  count_launch();
-  k_plan<<<1, sb, sb * sizeof(int32_t), st>>>(offsets, E, max_n, tile_prefix, tile_rows, sched);
-  LP_CHECK_LAUNCH("k_plan");
+  LP_CUDA(launch_pdl(k_plan, 1, sb, sb * sizeof(int32_t), st, offsets, E, max_n, tile_prefix, tile_rows, sched));
   if ((rc = launch_experts(x_perm, S, nullptr, S, w13, w2, H, I, E, max_n, offsets, tile_prefix, tile_rows, sched,
                            act, y_perm,
                            st)))
@@ -1100,7 +1100,6 @@ size_t lp_ep_ctl_bytes(int P, int E) {
 int lp_ep_barrier(uint32_t* const* peer_ctl, int P, int rank, void* stream) {
   if (P < 1 || P > lp::kEpMaxRanks || rank < 0 || rank >= P || !peer_ctl)
     return fail(LP_EINVAL, "lp_ep_barrier: bad arguments P=%d rank=%d", P, rank);
-  count_launch();
   LP_CUDA(launch_pdl(lp::k_ep_barrier, 1, 32, 0, static_cast<cudaStream_t>(stream), peer_ctl, P, rank));
   return ok();
 }
@@ -1112,7 +1111,6 @@ int lp_ep_exchange(const int32_t* counts, uint32_t* const* peer_ctl, int P, int 
     return fail(LP_EINVAL, "lp_ep_exchange: bad arguments P=%d El=%d rank=%d", P, El, rank);
   const size_t sm = static_cast<size_t>(P) * P * El * sizeof(int32_t);
   if (sm > 48 * 1024) return fail(LP_EUNSUPPORTED, "lp_ep_exchange: P*P*El too large");
-  count_launch();
   const int threads = 256;  // one thread per global expert (P * El <= 256) for the plan's block scan
   LP_CUDA(launch_pdl(lp::k_ep_exchange, 1, threads, sm, static_cast<cudaStream_t>(stream), counts, peer_ctl, P, El,
                      rank, dest_base, off_local, rows_out));
@@ -1128,7 +1126,6 @@ int lp_ep_dispatch(const void* x, const int32_t* ids, const int32_t* slot_of, co
     return fail(LP_EINVAL, "lp_ep_dispatch: null pointer argument");
   if (!aligned16(x)) return fail(LP_EINVAL, "lp_ep_dispatch: x must be 16-byte aligned");
   const int S = T * topk;
-  count_launch();
   LP_CUDA(launch_pdl(lp::k_ep_dispatch, (S + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream),
                      static_cast<const __nv_bfloat16*>(x), ids, slot_of, offsets, dest_base,
                      reinterpret_cast<__nv_bfloat16* const*>(peer_recv), S, H, topk, El, dest_rank, dest_row));
@@ -1141,7 +1138,6 @@ int lp_ep_combine(void* const* peer_y, const int32_t* dest_rank, const int32_t* 
   if (T == 0) return ok();
   if (!peer_y || !dest_rank || !dest_row || !w || !y) return fail(LP_EINVAL, "lp_ep_combine: null pointer argument");
   if (!aligned16(y)) return fail(LP_EINVAL, "lp_ep_combine: y must be 16-byte aligned");
-  count_launch();
   LP_CUDA(launch_pdl(lp::k_ep_combine, T, 256, 0, static_cast<cudaStream_t>(stream),
                      reinterpret_cast<__nv_bfloat16* const*>(peer_y), dest_rank, dest_row, w, T, topk, H,
                      static_cast<__nv_bfloat16*>(y)));
