@@ -809,7 +809,11 @@ int lp_moe_route(const void* x, const void* wr, int T, int H, int E, int topk, i
   if (!aligned16(x) || !aligned16(wr)) return fail(LP_EINVAL, "lp_moe_route: x/wr must be 16-byte aligned");
   const Layout L = make_layout(T, H, 128, E, topk);
   if (ws_bytes < L.ids) return fail(LP_EINVAL, "lp_moe_route: workspace %zu < %zu bytes", ws_bytes, L.ids);
-  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, static_cast<cudaStream_t>(stream)))) return rc;
+  // no per-tile histogram: a standalone lp_moe_permute recomputes what it needs from the ids
+  // (k_scan_slots, or k_chunk_hist on the chunked path), so the router's would never be read
+  if ((rc = launch_route(x, wr, T, H, E, topk, renorm, ids, w, ws, L, static_cast<cudaStream_t>(stream), nullptr,
+                         nullptr, 0, false)))
+    return rc;
   return ok();
 }
 
