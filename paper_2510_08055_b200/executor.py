@@ -32,7 +32,7 @@ import torch.distributed as dist
 
 from .moe import GpuMoE, Workspace, add_rmsnorm
 from .synthetic import router_weight
-from .types import MoEShape
+from .types import MoEShape, require
 
 
 class _DecodeGraphs:
@@ -317,7 +317,8 @@ class AttentionDense:
 
     HEADS, KV_HEADS, HEAD_DIM = 32, 4, 128
 
-    def __init__(self, hidden: int, num_layers: int, device, seed: int = 0, std: float = 0.02):
+    def __init__(self, hidden: int, num_layers: int, device, seed: int = 0, std: float = 0.02,
+                 pool_slots: int = 0, pool_len: int = 0):
         self.H, self.L = hidden, num_layers
         self.device = torch.device(device)
         qd, kd = self.HEADS * self.HEAD_DIM, self.KV_HEADS * self.HEAD_DIM
@@ -328,25 +329,73 @@ class AttentionDense:
         self.wo = [(torch.randn((hidden, qd), generator=g, device=self.device) * std).to(torch.bfloat16)
                    for _ in range(num_layers)]
         self.kv: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        # pooled KV (pool_slots > 0): every request's cache is a slot of one [L, slots, pool_len, 4, 128]
+        # tensor, so a decode step's rows (any mix of context lengths) write and read their KV with a
+        # few indexed ops and ONE padded, masked SDPA call per layer instead of per-request work
+        self.Kp = self.Vp = None
+        if pool_slots > 0:
+            shape = (num_layers, pool_slots, pool_len, self.KV_HEADS, self.HEAD_DIM)
+            # zero-filled: masked-out positions get softmax weight 0, and 0 x (uninitialised NaN) is NaN
+            self.Kp = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+            self.Vp = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+            self.arange = torch.arange(pool_len, device=self.device)
+            self.free = list(range(pool_slots - 1, -1, -1))
+            self.slot: dict[int, int] = {}
+            self.pool_len = pool_len
+        self._plan_key = None
+        self._plan = None
 
     def cache(self, rid: int, length: int):
         c = self.kv.get(rid)
         if c is None:
-            shape = (self.L, length, self.KV_HEADS, self.HEAD_DIM)
-            c = (torch.empty(shape, dtype=torch.bfloat16, device=self.device),
-                 torch.empty(shape, dtype=torch.bfloat16, device=self.device))
+            if self.Kp is not None:
+                require(length <= self.pool_len and self.free, "AttentionDense: KV pool exhausted")
+                sl = self.free.pop()
+                self.slot[rid] = sl
+                c = (self.Kp[:, sl], self.Vp[:, sl])
+            else:
+                shape = (self.L, length, self.KV_HEADS, self.HEAD_DIM)
+                c = (torch.empty(shape, dtype=torch.bfloat16, device=self.device),
+                     torch.empty(shape, dtype=torch.bfloat16, device=self.device))
             self.kv[rid] = c
         return c
 
     def drop(self, rid: int) -> None:
-        self.kv.pop(rid, None)
+        if self.kv.pop(rid, None) is not None and self.Kp is not None:
+            self.free.append(self.slot.pop(rid))
+
+    def pool_plan(self, spans: list):
+        """Host side of the pooled decode step: (B, slots, positions, ctx) of the leading run of one-row
+        spans (a one-token prefill chunk at position p computes exactly what a decode row does), with
+        a slot assigned to every new request; ctx is the longest context rounded up to 128 (fewer
+        distinct attention shapes), positions past a row's own are masked."""
+        dec = []
+        for sp in spans:
+            if sp[2] != 1:
+                break
+            dec.append(sp)
+        for sp in dec:
+            self.cache(sp[0], sp[3])
+        if not dec:
+            return 0, [], [], 0
+        ctx = min(self.pool_len, -(-(max(sp[1] for sp in dec) + 1) // 128) * 128)
+        return len(dec), [self.slot[sp[0]] for sp in dec], [sp[1] for sp in dec], ctx
+
+    def _decode_plan(self, spans: list):
+        """Device index tensor [2, B] (slots; positions) of pool_plan, built once per segment."""
+        if self._plan_key is spans:
+            return self._plan
+        B, slots, pos, ctx = self.pool_plan(spans)
+        plan = (B, torch.tensor([slots, pos], device=self.device), ctx) if B else None
+        self._plan_key, self._plan = spans, plan
+        return plan
 
     def _heads(self, t: torch.Tensor) -> torch.Tensor:
         """[B, 4, ctx, 128] KV heads -> [B, 32, ctx, 128] (GQA by repetition: SDPA's fused backends then
         take the lower-right causal bias; with enable_gqa some shapes fell back to the math path)."""
         return t.repeat_interleave(self.HEADS // self.KV_HEADS, dim=1)
 
-    def layer(self, l: int, h: torch.Tensor, spans: list) -> None:
+    def layer(self, l: int, h: torch.Tensor, spans: list, plan=None) -> None:
         """h [T, H] (in place) += Wo · attention(QKV(RMSNorm(h))); spans: (rid, pos0, n, cache_len) per
         consecutive row run, decode rows first (n = 1), in row order."""
         import torch.nn.functional as F
@@ -358,9 +407,9 @@ class AttentionDense:
         order = [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION,
                  SDPBackend.MATH]
         with sdpa_kernel(order, set_priority=True):
-            self._layer(F, l, h, T, spans)
+            self._layer(F, l, h, T, spans, plan)
 
-    def _layer(self, F, l: int, h: torch.Tensor, T: int, spans: list) -> None:
+    def _layer(self, F, l: int, h: torch.Tensor, T: int, spans: list, plan=None) -> None:
         xn = torch.empty_like(h)
         add_rmsnorm(h, None, xn)
         qkv = xn @ self.wqkv[l].t()
@@ -370,6 +419,22 @@ class AttentionDense:
         out = torch.empty((T, self.HEADS, self.HEAD_DIM), dtype=h.dtype, device=h.device)
         row = 0
         i = 0
+        if self.Kp is not None:  # pooled: every decode row (leading spans) in one masked SDPA call
+            if plan is None:
+                plan = self._decode_plan(spans)
+            if plan is not None:
+                B, idx, ctx = plan
+                slots, pos = idx[0], idx[1]
+                mask = (self.arange[:ctx][None, :] <= pos[:, None])[:, None, None, :]     # [B, 1, 1, ctx]
+                self.Kp[l, slots, pos] = k[:B]
+                self.Vp[l, slots, pos] = v[:B]
+                # GQA without repeating K/V: the 8 query heads of a KV head are 8 query rows of it
+                qg = q[:B].view(B, self.KV_HEADS, self.HEADS // self.KV_HEADS, self.HEAD_DIM)
+                kb = self.Kp[l, slots, :ctx].transpose(1, 2)                        # [B, 4, ctx, 128]
+                vb = self.Vp[l, slots, :ctx].transpose(1, 2)
+                o = F.scaled_dot_product_attention(qg, kb, vb, attn_mask=mask)     # [B, 4, 8, 128]
+                out[:B] = o.reshape(B, self.HEADS, self.HEAD_DIM)
+                row = i = B
         while i < len(spans):
             rid, pos0, n, clen = spans[i]
             if n == 1:  # a run of decode rows at the same position: one batched SDPA
@@ -410,14 +475,86 @@ class AttentionDense:
         h += out.view(T, self.qd) @ self.wo[l].t()
 
 
+class _IterationGraphs:
+    """CUDA graphs of whole decode-only iterations in measured-attention mode: for every layer,
+    pooled-KV attention + dense projections (AttentionDense) and then the MoE sublayer, all L layers
+    in one graph, captured once per (decode rows, context bucket) on static buffers and replayed.
+    Eagerly a decode iteration is ~16 small launches per layer, and the host cost of issuing them
+    (~350 us per layer) would be what the engine's device-timed iteration measures; replay keeps it
+    device-bound. The MoE layers run on their own fixed workspace (the stack's shared one grows for
+    prefill batches, which would move its address under a captured graph)."""
+
+    def __init__(self, stack: "MoEModel", att: AttentionDense, max_rows: int):
+        require(att.Kp is not None, "iteration graphs need AttentionDense(pool_slots > 0)")
+        self.stack, self.att, self.max_rows = stack, att, max_rows
+        s = stack.shape
+        self.workspace = Workspace(stack.device)
+        self.layers = [GpuMoE(s, m.wr, m.w13, m.w2, workspace=self.workspace) for m in stack.layers]
+        self.workspace.get(max(self.layers[0].workspace_bytes(t) for t in range(1, max_rows + 1)))
+        for layer in self.layers:
+            layer._bufs(max_rows)
+        self.pool = torch.cuda.graph_pool_handle()
+        self.graphs: dict[tuple, tuple] = {}
+
+    def _step(self, x, xn, y, c, plan) -> None:
+        for l in range(self.stack.num_layers):
+            self.att.layer(l, x, [], plan)
+            add_rmsnorm(x, None, xn)
+            self.layers[l](xn, out=y, counts_out=c[l])
+            add_rmsnorm(x, y, xn)
+
+    def _graph(self, B: int, ctx: int):
+        key = (B, ctx)
+        g = self.graphs.get(key)
+        if g is None:
+            dev, H = self.stack.device, self.stack.shape.hidden
+            x = torch.zeros((B, H), dtype=torch.bfloat16, device=dev)
+            xn, y = torch.zeros_like(x), torch.zeros_like(x)
+            c = torch.zeros((self.stack.num_layers, self.stack.shape.num_experts), dtype=torch.int32, device=dev)
+            idx = torch.zeros((2, B), dtype=torch.int64, device=dev)
+            plan = (B, idx, ctx)
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                # warm-up outside the capture (attention plans, kernel attributes) on slot 0 / position
+                # 0 of the zero inputs: the replay that follows rewrites every KV row it reads
+                kp0, vp0 = self.att.Kp[:, :1, :1].clone(), self.att.Vp[:, :1, :1].clone()
+                self._step(x, xn, y, c, plan)
+                graph.capture_begin(pool=self.pool)
+                self._step(x, xn, y, c, plan)
+                graph.capture_end()
+                self.att.Kp[:, :1, :1] = kp0
+                self.att.Vp[:, :1, :1] = vp0
+            torch.cuda.current_stream(dev).wait_stream(side)
+            g = (graph, x, c, idx)
+            self.graphs[key] = g
+        return g
+
+    def run(self, dec: torch.Tensor, slots: list, pos: list, ctx: int, counts: torch.Tensor, events: list):
+        graph, x, c, idx = self._graph(dec.shape[0], ctx)
+        idx.copy_(torch.tensor([slots, pos], dtype=torch.int64), non_blocking=False)
+        x.copy_(dec)
+        e0, e1 = _timed(events)
+        e0.record()
+        graph.replay()
+        e1.record()
+        counts += c
+        return x.clone()
+
+
 class LayeredExecutor:
     """Runs a reference `BatchPlan` on the resident layer stack (duck-typed on moesim's SimState:
     `state.request(rid)` with `input_len` and `phase`)."""
 
     def __init__(self, stack: MoEModel, embed_seed: int = 0, keep_final_prompt: bool = False,
-                 attention: AttentionDense | None = None):
+                 attention: AttentionDense | None = None, iteration_graphs: int = 0):
         self.stack = stack
         self.attention = attention  # measured attention + dense projections (None: modelled by the reference)
+        # decode-only iterations of up to this many rows replay one CUDA graph of all layers
+        # (measured attention with a pooled KV cache; single-GPU stack)
+        self.igraphs = (_IterationGraphs(stack, attention, iteration_graphs)
+                        if iteration_graphs > 0 and attention is not None else None)
         self.keep_final_prompt = keep_final_prompt
         self.final_prompt: dict[int, torch.Tensor] = {}
         self.final_decode: dict[int, torch.Tensor] = {}  # last decode hidden row of finished requests
@@ -449,6 +586,11 @@ class LayeredExecutor:
             rows.append(row)
         return rows
 
+    @staticmethod
+    def _decode_span(state, rid: int) -> tuple:
+        r = state.request(rid)  # the decode row is the token at position input_len + emitted - 1
+        return rid, r.input_len + r.tokens_emitted - 1, 1, r.input_len + r.output_len
+
     def run_plan(self, state, plan) -> MoEIteration:
         L = self.stack.num_layers
         if self.attention is not None:  # KV caches of requests the engine retired since the last call
@@ -469,6 +611,12 @@ class LayeredExecutor:
                 routed[layer] += a.num_tokens
         events, attn_events = [], []
         dec = torch.stack(dec_rows) if D else torch.empty((0, self.H), dtype=torch.bfloat16, device=self.dev)
+        graphed = False
+        if self.igraphs is not None and 0 < D <= self.igraphs.max_rows and not plan.prefill_assignments:
+            spans = [self._decode_span(state, rid) for rid in plan.decode_ids]
+            B, slots, pos, ctx = self.attention.pool_plan(spans)
+            dec = self.igraphs.run(dec, slots, pos, ctx, counts, events)
+            graphed, cuts = True, []
         for l0, l1 in zip(cuts, cuts[1:]):
             act = [a for a in plan.prefill_assignments if a.layer_start <= l0 < a.layer_end]
             parts = [dec] + [self._prompt(state, a.request_id)[a.token_start:a.token_end] for a in act]
@@ -480,8 +628,7 @@ class LayeredExecutor:
                 # expert-parallel stack's row gather): the stack records the events
                 x = self.stack.run_segment(x, l0, l1, counts, events)
             else:  # per layer: attention + dense (measured), then the MoE sublayer
-                spans = [(rid, state.request(rid).input_len + state.request(rid).tokens_emitted - 1, 1,
-                          state.request(rid).input_len + state.request(rid).output_len) for rid in plan.decode_ids]
+                spans = [self._decode_span(state, rid) for rid in plan.decode_ids]
                 spans += [(a.request_id, a.token_start, a.num_tokens,
                            state.request(a.request_id).input_len + state.request(a.request_id).output_len)
                           for a in act]
@@ -509,7 +656,8 @@ class LayeredExecutor:
         nnz = (self.stack.reduce_counts(counts) > 0).sum(dim=1).cpu().tolist()
         self.iter_log.append({"moe_s": moe_s, "routed": routed, "experts_hit": nnz, "decode": D,
                               "prefill_tokens": plan.prefill_tokens,
-                              "attn_s": sum(a.elapsed_time(b) for a, b in attn_events) * 1e-3})
+                              "attn_s": sum(a.elapsed_time(b) for a, b in attn_events) * 1e-3,
+                              "graphed": graphed})
         # drop finished requests' state (the engine retires them after this call)
         live = set(plan.decode_ids) | {r.id for r in state.decoding}
         for rid in [k for k in self.decode_row if k not in live]:

@@ -193,6 +193,33 @@ def test_attention_dense_chunks_and_decode_match_fp32(cuda):
     assert err < 1e-2, err
 
 
+def test_attention_pooled_kv_matches_per_request(cuda):
+    """Pooled KV mode (one masked SDPA for every decode row, mixed context lengths) gives the rows the
+    per-request caches give: three prompts of different lengths, then two decode steps of all three."""
+    from paper_2510_08055_b200.executor import AttentionDense
+
+    outs = []
+    for pool in (0, 4):
+        att = AttentionDense(256, 2, cuda, seed=5, pool_slots=pool, pool_len=64)
+        g = torch.Generator(device=cuda).manual_seed(4)
+        lens = {1: 9, 2: 17, 3: 30}
+        rows = []
+        for rid, n in lens.items():
+            x = torch.randn((n, 256), generator=g, device=cuda).to(torch.bfloat16)
+            att.layer(0, x, [(rid, 0, n, 40)])
+            rows.append(x)
+        for step in range(2):
+            d = torch.randn((3, 256), generator=g, device=cuda).to(torch.bfloat16)
+            att.layer(0, d, [(rid, n + step, 1, 40) for rid, n in lens.items()])
+            rows.append(d)
+        att.drop(2)
+        outs.append(torch.cat(rows).float())
+        if pool:
+            assert att.free == [3, 1]  # slot of request 2 returned
+    err = ((outs[0] - outs[1]).norm() / outs[0].norm()).item()
+    assert err < 1e-2, err
+
+
 def test_layered_vs_chunked_with_measured_attention(stack):
     """With measured attention + dense projections the reference engine's layered and chunked runs
     reach the same final prompt hidden states (bf16: different chunking gives different rounding,
@@ -212,3 +239,26 @@ def test_layered_vs_chunked_with_measured_attention(stack):
     for rid in range(2):
         a, b = out["layered"].final_prompt[rid].float(), out["chunked"].final_prompt[rid].float()
         assert ((a - b).norm() / a.norm()).item() < 3e-2, rid
+
+
+def test_iteration_graphs_match_eager_pooled_attention(stack):
+    """Decode-only iterations replayed as one CUDA graph of every layer (pooled-KV attention + MoE)
+    reach the decode rows the eager per-layer calls reach, bit for bit."""
+    from paper_2510_08055_b200.executor import AttentionDense
+
+    reqs = _reqs((300, 200, 100), 6)
+    out = {}
+    for graphs in (0, 8):
+        att = AttentionDense(TINY.hidden, 4, stack.device, seed=9, pool_slots=3, pool_len=320)
+        ex = LayeredExecutor(stack, keep_final_prompt=True, attention=att, iteration_graphs=graphs)
+        with refdrive.measured_costs(executor=ex):
+            ms.engine.run(TINY_MODEL, refdrive.b200_hardware(), _cfg("layered"), reqs, _table())
+        n = sum(it["graphed"] for it in ex.iter_log)
+        assert (n > 0) == (graphs > 0), n
+        assert all(it["moe_s"] > 0 for it in ex.iter_log)
+        out[graphs] = ex
+    for rid in range(3):
+        # the last iteration's rows stay in decode_row (no later call retires them)
+        a, b = (out[g].final_decode.get(rid, out[g].decode_row.get(rid)) for g in (0, 8))
+        assert a.abs().max().item() > 0
+        assert torch.equal(a, b), (rid, (a.float() - b.float()).abs().max().item())

@@ -49,14 +49,24 @@ def _h100():
 
 
 ATTENTION = False  # --attention: measured attention + dense projections (executor.AttentionDense)
+IGRAPHS = True  # --attention + pooled KV: decode-only iterations replay one CUDA graph of all layers
+KV_POOL = True  # --attention: one pooled KV tensor, one masked SDPA for all decode rows (--no-kv-pool: per request)
 
 
 def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, graphs=0):
     from paper_2510_08055_b200.executor import AttentionDense, LayeredExecutor
 
     cfg = ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=chunk, group_token_target=target)
-    att = AttentionDense(QWEN3_30B_A3B.hidden, MODEL.num_layers, stack.device, seed=11) if ATTENTION else None
-    ex = LayeredExecutor(stack, attention=att)
+    att = None
+    if ATTENTION:
+        # pooled KV: one slot per request, each as long as the longest request, when that fits 48 GB
+        # (C3: 33 x 8208 positions = 27 GB); otherwise per-request caches
+        plen = max(r.input_len + r.output_len for r in reqs)
+        slots = len(reqs) if KV_POOL and len(reqs) * plen * MODEL.num_layers * 4 * 128 * 2 * 2 <= 48e9 else 0
+        att = AttentionDense(QWEN3_30B_A3B.hidden, MODEL.num_layers, stack.device, seed=11,
+                             pool_slots=slots, pool_len=plen)
+    ex = LayeredExecutor(stack, attention=att,
+                         iteration_graphs=64 if att is not None and att.Kp is not None and IGRAPHS else 0)
     t0 = time.time()
     with refdrive.measured_costs(executor=ex):
         res = ms.engine.run(MODEL, refdrive.b200_hardware(), cfg, reqs, ms.coverage.EmpiricalTable())
@@ -68,6 +78,7 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
            "moe_us_per_layer_call": 1e6 * moe_s / max(1, sum(sum(1 for n in it["routed"] if n)
                                                              for it in ex.iter_log)),
            "decode_graph_tokens": graphs, "wall_s": wall,
+           "kv_pool_slots": att.Kp.shape[1] if att is not None and att.Kp is not None else 0,
            "measured": "MoE + attention + dense projections (attention: PyTorch SDPA, dense: cuBLAS)" if ATTENTION
            else "MoE (attention / dense projections: the reference's roofline model on B200 peaks)"}
     if focus is not None:
@@ -88,7 +99,9 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
                                                      "num_iterations")}
     out["gpus"] = getattr(stack, "world", 1)
     if ATTENTION:
+        # eager iterations only (a graphed decode iteration is timed as a whole, in moe_time_ms)
         out["attention_dense_ms"] = 1e3 * sum(it["attn_s"] for it in ex.iter_log)
+        out["graphed_iterations"] = sum(it.get("graphed", False) for it in ex.iter_log)
     if emit and EMIT:
         print(json.dumps(out), flush=True)
     return out
@@ -110,6 +123,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1, help="expert-parallel ranks (one per GPU)")
     ap.add_argument("--attention", action="store_true",
                     help="measure attention + dense projections too (library kernels; single GPU)")
+    ap.add_argument("--no-iteration-graphs", action="store_true", help="--attention: eager decode iterations")
+    ap.add_argument("--no-kv-pool", action="store_true", help="--attention: per-request KV caches")
     ap.add_argument("--max-tokens", type=int, default=40960,
                     help="--gpus > 1: the largest segment (rows of one layer call, all ranks) to size EP buffers")
     a = ap.parse_args()
@@ -125,8 +140,10 @@ def main():
                                   os.path.abspath(__file__), *sys.argv[1:]]))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    global ATTENTION
+    global ATTENTION, KV_POOL, IGRAPHS
     ATTENTION = a.attention
+    KV_POOL = not a.no_kv_pool
+    IGRAPHS = not a.no_iteration_graphs
     if ATTENTION and world > 1:
         raise SystemExit("serving_bench.py: --attention is a single-GPU mode")
     if world != a.gpus:
