@@ -117,6 +117,12 @@ class _DecodeGraphs:
 class MoEModel:
     """`num_layers` resident MoE layers of `shape` with random-init weights."""
 
+    # tokens per lp_moe_forward call: a layered-prefill cohort can hold hundreds of thousands of prompt
+    # tokens (C5 with measured attention reached 400 K), above the C-ABI's T limit and the x_perm /
+    # y_perm workspace worth keeping; larger segments run each layer in row slices (per-token math,
+    # so the rows are bit-identical to one call)
+    max_call_tokens = 65536
+
     def __init__(self, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0, std: float = 0.02,
                  graph_tokens: int = 0):
         self.shape, self.num_layers = shape, num_layers
@@ -144,9 +150,17 @@ class MoEModel:
         y = torch.empty_like(x)
         c = torch.empty((l1 - l0, self.shape.num_experts), dtype=torch.int32, device=self.device)
         delta = None
+        M = self.max_call_tokens
+        part = torch.empty((self.shape.num_experts,), dtype=torch.int32, device=self.device) if T > M else None
         for i, layer in enumerate(range(l0, l1)):
             add_rmsnorm(x, delta, xn)
-            self.layers[layer](xn, out=y, counts_out=c[i])
+            if part is None:
+                self.layers[layer](xn, out=y, counts_out=c[i])
+            else:
+                c[i].zero_()
+                for r0 in range(0, T, M):
+                    self.layers[layer](xn[r0:r0 + M], out=y[r0:r0 + M], counts_out=part)
+                    c[i] += part
             delta = y
         if delta is not None and T:
             add_rmsnorm(x, delta, xn)

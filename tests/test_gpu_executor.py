@@ -103,6 +103,25 @@ def test_decode_graphs_match_eager(cuda):
         assert last[0] is not None and torch.equal(last[0], last[1]), rid
 
 
+def test_segments_above_the_call_limit_run_in_row_slices(stack):
+    """A segment larger than MoEModel.max_call_tokens (a layered-prefill cohort of many prompts)
+    runs each layer in row slices: hidden states and per-layer expert counts are bit-identical to
+    one call per layer."""
+    g = torch.Generator(device=stack.device).manual_seed(5)
+    x0 = torch.randn((1000, TINY.hidden), generator=g, device=stack.device).to(torch.bfloat16)
+    outs = []
+    for m in (MoEModel.max_call_tokens, 96):
+        stack.max_call_tokens = m
+        try:
+            counts = torch.zeros((4, TINY.num_experts), dtype=torch.int32, device=stack.device)
+            outs.append((stack.run_segment(x0.clone(), 0, 4, counts), counts))
+        finally:
+            del stack.max_call_tokens  # back to the class default
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert int(outs[0][1].sum()) == 4 * 1000 * TINY.top_k
+
+
 @pytest.fixture(scope="module")
 def qwen_layer(cuda):
     s = QWEN3_30B_A3B

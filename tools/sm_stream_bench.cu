@@ -72,6 +72,15 @@ __global__ void __launch_bounds__(64, 1) k_sm_stream(const __grid_constant__ CUt
   __syncthreads();
 }
 
+// keeps the stream busy while the host submits the timed launch: without it the first event is
+// stamped before the kernel is even submitted and every line carries ~5-7 us of host launch latency
+__global__ void k_spin(long long ns) {
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  long long t = t0;
+  while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+}
+
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
 template <int STAGES>
@@ -86,6 +95,7 @@ void run(const CUtensorMap& tm, int ctas, int kb_per_cta, int hot = 0, int boxes
   long long base = 0;
   for (int rep = 0; rep < reps; ++rep) {
     if (base + rows_per_launch > kRows) base = 0;
+    if (getenv("SPIN")) k_spin<<<1, 32>>>(50000);
     cudaEventRecord(a);
     k_sm_stream<STAGES><<<ctas, 64, smem>>>(tm, kb_per_cta, hot ? 0 : base, hot, boxes);
     cudaEventRecord(b);
