@@ -52,8 +52,6 @@ struct DecodeCfg {
   static constexpr int kMaxT = 16;
   static constexpr int kMaxE = 128;    // one router m-tile
   static constexpr int kBBytes = kN * 128;
-  static constexpr int kStageBytes = kATileBytes + kBBytes;  // 18 KiB (1024-aligned)
-  static constexpr int kStages = 11;
   static constexpr int kAcc = 2;
   static constexpr int kTmemCols = 32;
   static constexpr int kXBytes = 64 * kN * 4;                // up values handed to the gate warps
@@ -63,16 +61,30 @@ struct DecodeCfg {
   // off[E+1] cnt[E] hit[E] tok[S] ent[S] slot[S] + per-warp counts [4][E] + 16 scalars
   // ... + routing weights w[S] + the fused combine's finished-token lists [2][kMaxT + 1] (+ padding)
   static constexpr int kPermBytes = 4 * ((kMaxE + 1) + 5 * kMaxE + 4 * kMaxE + 19 + kMaxE + 40);  // 16-B multiple
-  static constexpr int kBarBytes = 8 * (3 * kStages + 1 + 2 * kAcc + 2 * kRing) + 16 * kRing + 16;
-  // folded logits + top-k scratch alias ring stage 0: used only between the routing MMAs' completion
-  // and the first streaming load
-  static_assert(kLogitBytes + kTopBytes <= kStageBytes, "routing scratch fits one ring stage");
-  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kXBytes + kPartBytes + kPermBytes + kBarBytes;
   static constexpr int kExitWord = 1 + kMaxExperts + 8;  // sched word counting finished CTAs
   static constexpr int kUpDoneWord = 1 + kMaxExperts + 4;  // UP items finished (all experts)
 };
-static_assert(DecodeCfg::kSmemBytes <= 232448, "decode kernel shared memory");
 static_assert(DecodeCfg::kPermBytes % 16 == 0, "barrier / ring alignment");
+
+// The weight ring: KS k-blocks (64-wide K slices) per stage, laid out [A_0 .. A_{KS-1} | B_0 .. B_{KS-1}]
+// (16 KiB weight tile + 2 KiB token rows per k-block, every tile 1024-B aligned). A decode item's
+// stream is paced per STAGE (each one waits for its TMA, its MMAs and the tcgen05.commit that frees
+// it), not per byte: tools/sm_stream_bench.cu on a B200 with the same MMA consumer, 96 SMs x 512 KiB,
+// 11 x 16 KiB stages 40 GB/s per SM vs 5 x 32 KiB 51 GB/s (profiles/r02/probe/sm_stream_stage_size.txt).
+// KS = 2 (5 stages of 36 KiB) is the default; KS = 1 (11 stages of 18 KiB) the round-2 original.
+template <int KS>
+struct DecodeRing {
+  static constexpr int kStageBytes = KS * (kATileBytes + DecodeCfg::kBBytes);
+  static constexpr int kStages = KS == 1 ? 11 : 5;
+  static constexpr int kBOff = KS * kATileBytes;  // first token-row tile of a stage
+  static constexpr int kBarBytes = 8 * (3 * kStages + 1 + 2 * DecodeCfg::kAcc + 2 * kRing) + 16 * kRing + 16;
+  // folded logits + top-k scratch alias ring stage 0: used only between the routing MMAs' completion
+  // and the first streaming load
+  static_assert(DecodeCfg::kLogitBytes + DecodeCfg::kTopBytes <= kStageBytes, "routing scratch fits one ring stage");
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + DecodeCfg::kXBytes + DecodeCfg::kPartBytes +
+                                    DecodeCfg::kPermBytes + kBarBytes;
+  static_assert(kSmemBytes <= 232448, "decode kernel shared memory");
+};
 
 // hit experts' W2 below this many bytes is warmed in L2 during the UP phase
 constexpr size_t kW2WarmBytes = 40u << 20;
@@ -96,7 +108,6 @@ struct DecodeParams {
   int weights_evict_first;
   int warm_w2;             // 1: L2-prefetch the hit experts' W2 when small
   int dnc;                 // 1: block-diagonal DN + combine items when S <= 16 and every UP item fits one wave
-  int act_gather;          // 1: DN items' act rows copied by the gather warps (cp.async) instead of TMA
 };
 
 __device__ __forceinline__ void cluster_arrive_rel() {
@@ -111,7 +122,7 @@ __device__ __forceinline__ void cluster_wait_acq() { asm volatile("barrier.clust
 // CS: CTAs per cluster (2: pairs, always co-resident, every SM streams; 4: each CTA computes one
 // partial (half the Wr bytes per CTA, shorter routing), but 4-CTA clusters leave some SMs unused
 // on a B200 (GPC boundaries) — the host picks 4 for latency-bound tiny batches)
-template <int CS>
+template <int CS, int KS>
 __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     k_decode(const __grid_constant__ CUtensorMap tm_wr, const __grid_constant__ CUtensorMap tm_x,
              const __grid_constant__ CUtensorMap tm_w13h, const __grid_constant__ CUtensorMap tm_w2,
@@ -119,14 +130,18 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
              const __grid_constant__ CUtensorMap tm_w2r16, const __grid_constant__ CUtensorMap tm_w2r32,
              const __grid_constant__ CUtensorMap tm_w2r64, const DecodeParams p) {
   using C = DecodeCfg;
+  using R = DecodeRing<KS>;
   constexpr int kCl = CS;                 // CTAs per cluster
   constexpr int kPpc = C::kParts / CS;    // partial sums per CTA
   static_assert(kPpc <= C::kMaxPpc, "partials per CTA");
-  constexpr int S_ = C::kStages;
+  constexpr int S_ = R::kStages;
   constexpr int A_ = C::kAcc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* cur = smem + S_ * C::kStageBytes;
+  uint8_t* cur = smem + S_ * R::kStageBytes;
+  // k-block h of ring stage st: weight tile / token-row tile
+  auto a_at = [&](int st, int h) { return smem + st * R::kStageBytes + h * kATileBytes; };
+  auto b_at = [&](int st, int h) { return smem + st * R::kStageBytes + R::kBOff + h * C::kBBytes; };
   float* xbuf = reinterpret_cast<float*>(cur);        cur += C::kXBytes;     // [16 cols][64 lanes]
   float* s_part = reinterpret_cast<float*>(cur);      cur += C::kPartBytes;  // [ppc][16 tokens][128 experts]
   float* s_logit = reinterpret_cast<float*>(smem);                           // [16][128] (ring stage 0)
@@ -189,71 +204,72 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
   int acc = 0; uint32_t aph = 0;      // TMEM accumulators (MMA / epilogue)
 
   // =============================== routing: partial sum `cr` of the logits ===============================
+  const int nst_r = (kbr + KS - 1) / KS;  // ring stages of the routing item
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();
-      const int npre = kbr < S_ ? kbr : S_;
+      const int npre = nst_r < S_ ? nst_r : S_;
       for (int i = 0; i < npre; ++i) {  // Wr before griddepcontrol.wait: weights never depend on the predecessor
-        mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-        tma_load_2d(smem + i * C::kStageBytes, &tm_wr, &full[i], (cr * kbr + i) * kTileK, 0, pol);
+        const int nh = min(KS, kbr - i * KS);
+        mbar_arrive_expect_tx(&full[i], nh * (kATileBytes + C::kBBytes));
+        for (int h = 0; h < nh; ++h) tma_load_2d(a_at(i, h), &tm_wr, &full[i], (cr * kbr + i * KS + h) * kTileK, 0, pol);
       }
       pdl_wait();
       LP_TRACE_AT(tr, 54);
       for (int i = 0; i < npre; ++i)
-        tma_load_2d(smem + i * C::kStageBytes + kATileBytes, &tm_x, &full[i], (cr * kbr + i) * kTileK, 0, pol);
+        for (int h = 0; h < min(KS, kbr - i * KS); ++h)
+          tma_load_2d(b_at(i, h), &tm_x, &full[i], (cr * kbr + i * KS + h) * kTileK, 0, pol);
       stage = npre % S_;
       phase = npre == S_ ? 1u : 0u;
-      for (int i = npre; i < kbr; ++i) {
+      for (int i = npre; i < nst_r; ++i) {
+        const int nh = min(KS, kbr - i * KS);
         mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * C::kStageBytes;
-        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-        tma_load_2d(sa, &tm_wr, &full[stage], (cr * kbr + i) * kTileK, 0, pol);
-        tma_load_2d(sa + kATileBytes, &tm_x, &full[stage], (cr * kbr + i) * kTileK, 0, pol);
+        mbar_arrive_expect_tx(&full[stage], nh * (kATileBytes + C::kBBytes));
+        for (int h = 0; h < nh; ++h) {
+          tma_load_2d(a_at(stage, h), &tm_wr, &full[stage], (cr * kbr + i * KS + h) * kTileK, 0, pol);
+          tma_load_2d(b_at(stage, h), &tm_x, &full[stage], (cr * kbr + i * KS + h) * kTileK, 0, pol);
+        }
         if (++stage == S_) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, C::kN);
-      if (kbr <= S_) {
-        // every routing k-block fits the ring (all loads already in flight): wait for all of them,
+      // routing k-block kb of this CTA: partial (kb / kbp) accumulates in TMEM columns 16 * (kb / kbp)
+      auto mma_kb = [&](int st, int h, int kb) {
+        const uint64_t a0 = sdesc_kmajor_sw128(smem_u32(a_at(st, h)));
+        const uint64_t b0 = sdesc_kmajor_sw128(smem_u32(b_at(st, h)));
+        const uint32_t d = tmem_base + (kb / kbp) * C::kN;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((kb % kbp) | k) != 0);
+      };
+      if (nst_r <= S_) {
+        // every routing stage fits the ring (all loads already in flight): wait for all of them,
         // then issue the whole MMA chain back to back — a stage wait after an MMA issue costs the
         // issuing thread ~250 cycles (tools/mma_chain_bench.cu), so no wait sits between MMAs.
         // Same MMAs in the same order as below (bit-identical logits).
-        for (int i = 0; i < kbr; ++i) {
+        for (int i = 0; i < nst_r; ++i) {
           mbar_wait(&full[i], 0);
           mbar_wait(&bfull[i], 0);
         }
         tc_fence_after();
-        for (int i = 0; i < kbr; ++i) {
-          const uint32_t sa = smem_u32(smem + i * C::kStageBytes);
-          const uint64_t a0 = sdesc_kmajor_sw128(sa);
-          const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
-          const uint32_t d = tmem_base + (i / kbp) * C::kN;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((i % kbp) | k) != 0);
-        }
-        for (int i = 0; i < kbr; ++i) mma_commit(&empty[i]);
-        stage = kbr % S_;
-        phase = kbr == S_ ? 1u : 0u;
+        for (int kb = 0; kb < kbr; ++kb) mma_kb(kb / KS, kb % KS, kb);
+        for (int i = 0; i < nst_r; ++i) mma_commit(&empty[i]);
+        stage = nst_r % S_;
+        phase = nst_r == S_ ? 1u : 0u;
       }
-      for (int i = 0; i < (kbr <= S_ ? 0 : kbr); ++i) {  // partial (i / kbp) accumulates in TMEM columns 16 * (i / kbp)
+      for (int i = 0; i < (nst_r <= S_ ? 0 : nst_r); ++i) {
         mbar_wait(&full[stage], phase);
         mbar_wait(&bfull[stage], phase);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-        const uint64_t a0 = sdesc_kmajor_sw128(sa);
-        const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
-        const uint32_t d = tmem_base + (i / kbp) * C::kN;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((i % kbp) | k) != 0);
+        for (int h = 0; h < min(KS, kbr - i * KS); ++h) mma_kb(stage, h, i * KS + h);
         mma_commit(&empty[stage]);
         if (++stage == S_) { stage = 0; phase ^= 1; }
       }
       mma_commit(&tfull[0]);
     }
   } else if (warp == 2 || warp == 3) {
-    for (int i = 0; i < kbr; ++i) {  // routing operands come by TMA: keep bfull's phases in step
+    for (int i = 0; i < nst_r; ++i) {  // routing operands come by TMA: keep bfull's phases in step
       mbar_wait(&empty[stage], phase ^ 1);
       mbar_arrive(&bfull[stage]);
       cp_async_commit();  // one (empty) group per stage, as in the stream below
@@ -276,9 +292,9 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     mbar_arrive(&tempty[0]);
     if (tid == 128) LP_TRACE_AT(tr, 49);
   }
-  // ring / accumulator positions after the routing item (every role advanced through kbr stages)
-  stage = kbr % S_;
-  phase = (kbr / S_) & 1;
+  // ring / accumulator positions after the routing item (every role advanced through nst_r stages)
+  stage = nst_r % S_;
+  phase = (nst_r / S_) & 1;
   acc = 1;
   aph = 0;
   pdl_wait();
@@ -420,7 +436,6 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     }
     if (lane == 0) {
       const uint64_t pol_w = p.weights_evict_first ? policy_evict_first() : policy_evict_normal();
-      const uint64_t pol_a = policy_evict_last();
       int r = 0; uint32_t rph = 0;
       [[maybe_unused]] int n_item = 0;
       while (true) {
@@ -452,99 +467,32 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
         if (++r == kRing) { r = 0; rph ^= 1; }
         const int kind = info.x & 0xff;
         if (kind == kItemEnd) break;
-        const int e = info.x >> 8, m0 = info.y, row0 = info.z;
-        if (kind == kItemUp) {
-          LP_ITEM(n_item, 2, LP_NOW());
-          for (int kb = 0; kb < p.H / kTileK; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * C::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], kATileBytes);
-            // rows 0-63: gate features m0..m0+63, rows 64-127: the matching up rows
-            tma_load_2d(sa, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + m0, pol_w);
-            tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + p.I + m0, pol_w);
-            if (++stage == S_) { stage = 0; phase ^= 1; }
-          }
-        } else if (kind == kItemDnc) {
-          // W2 rows f0..f0+R-1 of every hit expert first, then all slots' act rows once every UP item is done
-          const CUtensorMap* tmr = rdnc == 8 ? &tm_w2r8 : rdnc == 16 ? &tm_w2r16 : rdnc == 32 ? &tm_w2r32
-                                   : rdnc == 64 ? &tm_w2r64 : &tm_w2;
-          const uint32_t abytes = static_cast<uint32_t>(nnz * rdnc * 128);
-          const int kblocks = p.I / kTileK;
-          const int npre = kblocks < S_ ? kblocks : S_;
-          const int st0 = stage;
-          if (p.act_gather) {  // the gather warps bring the act rows: weights only, no dependency here
-            LP_ITEM(n_item, 2, LP_NOW());
-            for (int kb = 0; kb < kblocks; ++kb) {
-              mbar_wait(&empty[stage], phase ^ 1);
-              uint8_t* sa = smem + stage * C::kStageBytes;
-              mbar_arrive_expect_tx(&full[stage], abytes);
-              for (int j = 0; j < nnz; ++j)
-                tma_load_2d(sa + j * rdnc * 128, tmr, &full[stage], kb * kTileK, s_hit[j] * p.H + m0, pol_w);
-              if (++stage == S_) { stage = 0; phase ^= 1; }
+        const int e = info.x >> 8, m0 = info.y;
+        // weight tiles only: UP token rows and DN / DNC act rows are copied by the gather warps
+        const int kblocks = kind == kItemUp ? p.H / kTileK : p.I / kTileK;
+        const CUtensorMap* tmr = kind != kItemDnc ? &tm_w2 : rdnc == 8 ? &tm_w2r8 : rdnc == 16 ? &tm_w2r16
+                                 : rdnc == 32 ? &tm_w2r32 : rdnc == 64 ? &tm_w2r64 : &tm_w2;
+        const uint32_t abytes = kind == kItemDnc ? static_cast<uint32_t>(nnz * rdnc * 128) : kATileBytes;
+        LP_ITEM(n_item, 2, LP_NOW());
+        for (int kb = 0; kb < kblocks; kb += KS) {
+          const int nh = min(KS, kblocks - kb);
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], nh * abytes);
+          for (int h = 0; h < nh; ++h) {
+            uint8_t* sa = a_at(stage, h);
+            const int kc = (kb + h) * kTileK;
+            if (kind == kItemUp) {
+              // rows 0-63: gate features m0..m0+63, rows 64-127: the matching up rows
+              tma_load_2d(sa, &tm_w13h, &full[stage], kc, e * 2 * p.I + m0, pol_w);
+              tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kc, e * 2 * p.I + p.I + m0, pol_w);
+            } else if (kind == kItemDnc) {
+              // W2 rows f0..f0+R-1 of every hit expert (block-diagonal A tile)
+              for (int j = 0; j < nnz; ++j) tma_load_2d(sa + j * rdnc * 128, tmr, &full[stage], kc, s_hit[j] * p.H + m0, pol_w);
+            } else {
+              tma_load_2d(sa, &tm_w2, &full[stage], kc, e * p.H + m0, pol_w);
             }
           }
-          for (int kb = 0; kb < (p.act_gather ? 0 : kblocks); ++kb) {
-            if (kb == npre) {
-              while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
-              fence_proxy_async_global();
-              LP_ITEM(n_item, 2, LP_NOW());
-              for (int k2 = 0, s2 = st0; k2 < npre; ++k2) {
-                tma_load_2d(smem + s2 * C::kStageBytes + kATileBytes, &tm_act, &full[s2], k2 * kTileK, 0, pol_a);
-                if (++s2 == S_) s2 = 0;
-              }
-            }
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * C::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], abytes + C::kBBytes);
-            for (int j = 0; j < nnz; ++j)
-              tma_load_2d(sa + j * rdnc * 128, tmr, &full[stage], kb * kTileK, s_hit[j] * p.H + m0, pol_w);
-            if (kb >= npre) tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, 0, pol_a);
-            if (++stage == S_) { stage = 0; phase ^= 1; }
-          }
-          if (!p.act_gather && npre == kblocks) {  // every k-block fitted the ring: act rows follow the dependency
-            while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
-            fence_proxy_async_global();
-            LP_ITEM(n_item, 2, LP_NOW());
-            for (int k2 = 0, s2 = st0; k2 < npre; ++k2) {
-              tma_load_2d(smem + s2 * C::kStageBytes + kATileBytes, &tm_act, &full[s2], k2 * kTileK, 0, pol_a);
-              if (++s2 == S_) s2 = 0;
-            }
-          }
-        } else if (p.act_gather) {
-          // W2 tiles only: the gather warps copy expert e's act rows once its UP items are done
-          LP_ITEM(n_item, 2, LP_NOW());
-          for (int kb = 0; kb < p.I / kTileK; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], kATileBytes);
-            tma_load_2d(smem + stage * C::kStageBytes, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
-            if (++stage == S_) { stage = 0; phase ^= 1; }
-          }
-        } else {
-          // W2 tiles first (they do not depend on the UP items), the act rows once expert e's act is final
-          const int kblocks = p.I / kTileK;
-          const int npre = kblocks < S_ ? kblocks : S_;
-          const int st0 = stage;
-          for (int kb = 0; kb < npre; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d(smem + stage * C::kStageBytes, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
-            if (++stage == S_) { stage = 0; phase ^= 1; }
-          }
-          while (ld_acquire_u32(&p.sched[1 + e]) < static_cast<uint32_t>(mt_up)) __nanosleep(32);
-          fence_proxy_async_global();
-          LP_ITEM(n_item, 2, LP_NOW());
-          for (int kb = 0, s = st0; kb < npre; ++kb) {
-            tma_load_2d(smem + s * C::kStageBytes + kATileBytes, &tm_act, &full[s], kb * kTileK, row0, pol_a);
-            if (++s == S_) s = 0;
-          }
-          for (int kb = npre; kb < kblocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * C::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
-            tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, row0, pol_a);
-            if (++stage == S_) { stage = 0; phase ^= 1; }
-          }
+          if (++stage == S_) { stage = 0; phase ^= 1; }
         }
         LP_ITEM(n_item, 3, LP_NOW());
         ++n_item;
@@ -565,14 +513,15 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
         const bool up = kind == kItemUp;
         const uint32_t idesc = idesc_bf16_f32(kTileM, (info.w + 15) & ~15);
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
+        const int nst = (kblocks + KS - 1) / KS;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C::kN;
 #ifndef LP_DECODE_MMA_BATCH
-#define LP_DECODE_MMA_BATCH 4  // B200: T=1 / 16 30.3 / 133.7-134.5 vs 30.8-31.1 / 136.6 us with 1
+#define LP_DECODE_MMA_BATCH 4  // k-blocks (B200, KS = 1: T=1 / 16 30.3 / 133.7-134.5 vs 30.8-31.1 / 136.6 us with 1)
 #endif
-        constexpr int MB = LP_DECODE_MMA_BATCH;  // stages waited for together, then issued back to back
-        for (int kb = 0; kb < kblocks; kb += MB) {
+        constexpr int MB = (LP_DECODE_MMA_BATCH + KS - 1) / KS;  // stages waited for together, then issued back to back
+        for (int s0 = 0; s0 < nst; s0 += MB) {
           int st[MB];
           uint32_t ph[MB];
 #pragma unroll
@@ -582,27 +531,29 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
           }
 #pragma unroll
           for (int g = 0; g < MB; ++g) {
-            if (kb + g < kblocks) {
+            if (s0 + g < nst) {
               mbar_wait(&full[st[g]], ph[g]);
               mbar_wait(&bfull[st[g]], ph[g]);
             }
           }
           tc_fence_after();
-          if (kb == 0) LP_ITEM(n_item, 5, LP_NOW());
+          if (s0 == 0) LP_ITEM(n_item, 5, LP_NOW());
 #pragma unroll
           for (int g = 0; g < MB; ++g) {
-            if (kb + g < kblocks) {
-              const uint32_t sa = smem_u32(smem + st[g] * C::kStageBytes);
-              const uint64_t a0 = sdesc_kmajor_sw128(sa);
-              const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
 #pragma unroll
-              for (int k = 0; k < kTileK / 16; ++k)
-                mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, ((kb + g) | k) != 0);
+            for (int h = 0; h < KS; ++h) {
+              const int kb = (s0 + g) * KS + h;
+              if (s0 + g < nst && kb < kblocks) {
+                const uint64_t a0 = sdesc_kmajor_sw128(smem_u32(a_at(st[g], h)));
+                const uint64_t b0 = sdesc_kmajor_sw128(smem_u32(b_at(st[g], h)));
+#pragma unroll
+                for (int k = 0; k < kTileK / 16; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+              }
             }
           }
 #pragma unroll
           for (int g = 0; g < MB; ++g) {
-            if (kb + g < kblocks) {
+            if (s0 + g < nst) {
               mma_commit(&empty[stage]);
               if (++stage == S_) { stage = 0; phase ^= 1; }
             }
@@ -616,11 +567,14 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 2 || warp == 3) {
-    // token-row gather for UP items (DN rows come by TMA): 16-byte cp.async into the SWIZZLE_128B layout
+    // B rows of every item, 16-byte cp.async into the SWIZZLE_128B layout: UP items' token rows
+    // (from x), DN / DNC items' act rows once the UP items they need are done (expert e's for DN,
+    // every expert's for DNC)
     constexpr int RPT = C::kN / 8;
     const int gt = tid - 64;
     const int g = gt >> 3, j = gt & 7;
     const uint64_t pol_x = policy_evict_last();
+    const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
     int r = 0; uint32_t rph = 0;
     while (true) {
       mbar_wait(&sfull[r], rph);
@@ -630,56 +584,41 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
       if (++r == kRing) { r = 0; rph ^= 1; }
       const int kind = info.x & 0xff;
       if (kind == kItemEnd) break;
-      if (kind == kItemUp) {
-        const int row0 = info.z, nvalid = info.w;
-        int tok[RPT];
+      const int row0 = info.z, nvalid = info.w;
+      const bool up = kind == kItemUp;
+      const int K_ = up ? p.H : p.I;  // row length of the source
+      const __nv_bfloat16* src0;
+      int rowi[RPT];  // source row of each copied tile row (-1: none)
+      if (up) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int rr = g + 8 * i;
-          tok[i] = rr < nvalid ? s_tok[row0 + rr] : -1;
+          rowi[i] = rr < nvalid ? s_tok[row0 + rr] : -1;
         }
-        const __nv_bfloat16* xs = p.x + j * 8;
-        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
-        for (int kb = 0; kb < p.H / kTileK; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          cp_async_wait_group<S_ - 1>();  // this slot's previous copies (S_ groups ago) landed
-          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + kATileBytes) + sw;
-#pragma unroll
-          for (int i = 0; i < RPT; ++i)
-            if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
-          cp_async_arrive_noinc(&bfull[stage]);
-          cp_async_commit();
-          if (++stage == S_) { stage = 0; phase ^= 1; }
-        }
-      } else if (p.act_gather) {
-        // DN / DNC items: this item's act rows [row0, row0 + nvalid) once the UP items they need are done
-        // (expert e's for DN, every expert's for DNC), 16-byte cp.async into the SWIZZLE_128B B stage
-        const int row0 = info.z, nvalid = info.w;
+        src0 = p.x + j * 8;
+      } else {
         // every lane acquires (its own cp.async reads are ordered after its own acquire)
         if (kind == kItemDnc)
           while (ld_acquire_u32(&p.sched[C::kUpDoneWord]) < static_cast<uint32_t>(n_up)) __nanosleep(32);
         else
           while (ld_acquire_u32(&p.sched[1 + (info.x >> 8)]) < static_cast<uint32_t>(mt_up)) __nanosleep(32);
-        const __nv_bfloat16* as = p.act + static_cast<size_t>(row0) * p.I + j * 8;
-        const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
-        for (int kb = 0; kb < p.I / kTileK; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          cp_async_wait_group<S_ - 1>();
-          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + kATileBytes) + sw;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) rowi[i] = g + 8 * i < nvalid ? g + 8 * i : -1;
+        src0 = p.act + static_cast<size_t>(row0) * p.I + j * 8;
+      }
+      const int kblocks = K_ / kTileK;
+      for (int kb = 0; kb < kblocks; kb += KS) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        cp_async_wait_group<S_ - 1>();  // this slot's previous copies (S_ groups ago) landed
+        for (int h = 0; h < min(KS, kblocks - kb); ++h) {
+          const uint32_t sb = smem_u32(b_at(stage, h)) + sw;
 #pragma unroll
           for (int i = 0; i < RPT; ++i)
-            if (g + 8 * i < nvalid) cp_async16(sb + i * 8 * 128, as + static_cast<size_t>(g + 8 * i) * p.I + kb * kTileK, pol_x);
-          cp_async_arrive_noinc(&bfull[stage]);
-          cp_async_commit();
-          if (++stage == S_) { stage = 0; phase ^= 1; }
+            if (rowi[i] >= 0) cp_async16(sb + i * 8 * 128, src0 + static_cast<size_t>(rowi[i]) * K_ + (kb + h) * kTileK, pol_x);
         }
-      } else {
-        for (int kb = 0; kb < p.I / kTileK; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive(&bfull[stage]);
-          cp_async_commit();
-          if (++stage == S_) { stage = 0; phase ^= 1; }
-        }
+        cp_async_arrive_noinc(&bfull[stage]);
+        cp_async_commit();
+        if (++stage == S_) { stage = 0; phase ^= 1; }
       }
     }
   } else {

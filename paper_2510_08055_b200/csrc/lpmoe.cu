@@ -586,8 +586,8 @@ int launch_experts_tiny(const void* x, const int32_t* tok_of, int S, const void*
 // disables. Knobs (B200, T=1 / 2 / 8 layer us, profiles/r02): LPMOE_DECODE_W2_WARM=1 L2-warms the hit
 // experts' W2 during the UP phase (off: 32.3 vs 34.2 at T=1 — it competes with the UP stream);
 // LPMOE_DECODE_DNC=0 disables the block-diagonal DN+combine items (on: 31.0 vs 31.9 at T=1);
-// LPMOE_DECODE_ACT_GATHER=0 loads DN act rows by TMA after the dependency instead of cp.async by
-// the gather warps (gather: 31.0 / 41.6 / 86.7 vs 32.8 / 41.9 / 91.7).
+// DN act rows are copied by the gather warps (cp.async; the TMA alternative measured 32.8 / 41.9 /
+// 91.7 vs 31.0 / 41.6 / 86.7 us and was removed). LPMOE_DECODE_KS=1 selects the 11 x 18 KiB ring.
 bool use_decode(int T, int H, int I, int E, int topk) {
   static const int v = env_int("LPMOE_DECODE", 1);
   return v != 0 && T >= 1 && T <= lp::DecodeCfg::kMaxT && T * topk <= E && E <= lp::DecodeCfg::kMaxE &&
@@ -600,7 +600,9 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
                   cudaStream_t st) {
   static const int warm = env_int("LPMOE_DECODE_W2_WARM", 0);
   static const int dnc = env_int("LPMOE_DECODE_DNC", 1);
-  static const int act_gather = env_int("LPMOE_DECODE_ACT_GATHER", 1);
+  // k-blocks per ring stage (decode_sm100.cuh DecodeRing): 2 = 5 stages of 36 KiB (default), 1 = 11 of 18 KiB
+  static const int ks_env = env_int("LPMOE_DECODE_KS", 2);
+  const int ks = ks_env == 1 ? 1 : 2;
   int rc;
   if ((rc = get_encode())) return rc;
   const int S = T * topk;
@@ -614,28 +616,28 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
   CUtensorMap tm_w2r[4];
   for (int i = 0; i < 4; ++i)
     if ((rc = make_tmap(&tm_w2r[i], w2, static_cast<uint64_t>(E) * H, I, 8u << i))) return rc;
-  constexpr int smem = lp::DecodeCfg::kSmemBytes;
+  const int smem = ks == 1 ? lp::DecodeRing<1>::kSmemBytes : lp::DecodeRing<2>::kSmemBytes;
   static const int forced_cs = env_int("LPMOE_DECODE_CS", 0);
   // B200 (profiles/r02/decode_cs.jsonl): 4-CTA clusters (132 SMs, half the Wr bytes per CTA) win at T <= 3
   // (T=1 30.6 vs 33.2 us, T=2 41.2 vs 44.5), pairs (148 SMs streaming) from T=4 (58.3 vs 60.1)
   const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 3 ? 4 : 2);
-  auto kern = cs == 4 ? lp::k_decode<4> : lp::k_decode<2>;
+  auto kern = cs == 4 ? (ks == 1 ? lp::k_decode<4, 1> : lp::k_decode<4, 2>)
+                      : (ks == 1 ? lp::k_decode<2, 1> : lp::k_decode<2, 2>);
   if ((rc = set_smem(kern, smem))) return rc;
   const lp::DecodeParams p{T, H, I, E, topk, renorm, static_cast<const __nv_bfloat16*>(x),
                            static_cast<const uint8_t*>(w2), ids, w, counts, offsets, slot_of, tok_of,
                            static_cast<__nv_bfloat16*>(act), static_cast<__nv_bfloat16*>(y_perm), sched,
-                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0, dnc != 0 ? 1 : 0,
-                           act_gather != 0 ? 1 : 0};
+                           static_cast<__nv_bfloat16*>(y), cmb, wpol, warm != 0 ? 1 : 0, dnc != 0 ? 1 : 0};
   // clusters of 4 that are co-resident (GPC boundaries can leave SMs that no 4-CTA cluster fits):
   // a second wave would repeat the routing prologue after the first wave's stream
   static std::mutex mu;
-  static int cached[64][2] = {};
+  static int cached[64][2][2] = {};
   int dev = 0;
   LP_CUDA(cudaGetDevice(&dev));
   int grid;
   {
     std::lock_guard<std::mutex> lock(mu);
-    int& g = cached[dev & 63][cs == 4];
+    int& g = cached[dev & 63][cs == 4][ks == 2];
     if (g <= 0) {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];

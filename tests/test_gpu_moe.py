@@ -306,7 +306,8 @@ def test_host_pipeline_matches_device_forward(cuda):
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
                                   "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0",
                                   "LPMOE_SCAN_SLOTS=0", "LPMOE_DECODE=0", "LPMOE_DECODE_W2_WARM=0",
-                                  "LPMOE_DECODE_COMBINE=0", "LPMOE_DECODE_CS=2", "LPMOE_DECODE_CS=4"])
+                                  "LPMOE_DECODE_COMBINE=0", "LPMOE_DECODE_CS=2", "LPMOE_DECODE_CS=4",
+                                  "LPMOE_DECODE_KS=1"])
 def test_experimental_paths_match_oracle(cuda, knob):
     """The env-selected alternative paths (off by default) stay bit-exact on routing and within tolerance."""
     import subprocess
