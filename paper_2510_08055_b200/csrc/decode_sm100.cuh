@@ -71,9 +71,12 @@ static_assert(DecodeCfg::kPermBytes % 16 == 0, "barrier / ring alignment");
 // stream is paced per STAGE (each one waits for its TMA, its MMAs and the tcgen05.commit that frees
 // it), not per byte: tools/sm_stream_bench.cu on a B200 with the same MMA consumer, 96 SMs x 512 KiB,
 // 11 x 16 KiB stages 40 GB/s per SM vs 5 x 32 KiB 51 GB/s (profiles/r02/probe/sm_stream_stage_size.txt).
-// KS = 2 (5 stages of 36 KiB) is the default; KS = 1 (11 stages of 18 KiB) the round-2 original.
+// KS = 2 (5 stages of 36 KiB) is the default; KS = 1 (11 stages of 18 KiB) the round-2 original; KS = 3
+// (3 stages of 54 KiB, all that fits) measured slower: T=1 / 8 / 16 33.4 / 99.6 / 150.0 vs 29.5 / 87.3 /
+// 132.3 us (profiles/r02/probe/bench_ks3.txt) — too few stages in flight.
 template <int KS>
 struct DecodeRing {
+  static_assert(KS == 1 || KS == 2, "k-blocks per stage");
   static constexpr int kStageBytes = KS * (kATileBytes + DecodeCfg::kBBytes);
   static constexpr int kStages = KS == 1 ? 11 : 5;
   static constexpr int kBOff = KS * kATileBytes;  // first token-row tile of a stage
