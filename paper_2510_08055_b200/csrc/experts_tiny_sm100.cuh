@@ -29,8 +29,12 @@ struct TinyCfg {
   static constexpr int kThreads = 256;
   static constexpr int kN = 16;                                   // token rows per item (MMA N)
   static constexpr int kBBytes = kN * 128;                        // 2 KiB
-  static constexpr int kStageBytes = kATileBytes + kBBytes;       // 18 KiB (1024-aligned)
-  static constexpr int kStages = 11;
+  // two k-blocks per ring stage, [A_0 | A_1 | B_0 | B_1] (36 KiB): the stream of a decode-size item is
+  // paced per stage, not per byte (decode_sm100.cuh DecodeRing, tools/sm_stream_bench.cu)
+  static constexpr int kKS = 2;
+  static constexpr int kStageBytes = kKS * (kATileBytes + kBBytes);
+  static constexpr int kBOff = kKS * kATileBytes;
+  static constexpr int kStages = 5;
   static constexpr int kAcc = 2;
   static constexpr int kTmemCols = 32;                            // 2 x 16 columns
   static constexpr int kXBytes = 64 * kN * 4;                     // up values handed to the gate warps
@@ -50,6 +54,9 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xbuf = reinterpret_cast<float*>(smem + S_ * C::kStageBytes);  // [16 cols][64 lanes]
+  constexpr int KS = C::kKS;
+  auto a_at = [&](int st, int h) { return smem + st * C::kStageBytes + h * kATileBytes; };
+  auto b_at = [&](int st, int h) { return smem + st * C::kStageBytes + C::kBOff + h * C::kBBytes; };
   uint8_t* aux = smem + S_ * C::kStageBytes + C::kXBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + S_;
@@ -144,16 +151,20 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
         LP_ITEM(n_item, 2, LP_NOW());
         const int kblocks = up ? p.H / kTileK : p.I / kTileK;
         const uint32_t bytes = kATileBytes + (up ? 0 : C::kBBytes);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb0 = 0; kb0 < kblocks; kb0 += KS) {
+          const int nh = min(KS, kblocks - kb0);
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          if (up) {  // rows 0-63: gate features m0..m0+63, rows 64-127: the matching up rows
-            tma_load_2d(sa, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + m0, pol_w);
-            tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kb * kTileK, e * 2 * p.I + p.I + m0, pol_w);
-          } else {
-            tma_load_2d(sa, &tm_w2, &full[stage], kb * kTileK, e * p.H + m0, pol_w);
-            tma_load_2d(sa + kATileBytes, &tm_act, &full[stage], kb * kTileK, row0, pol_a);
+          mbar_arrive_expect_tx(&full[stage], nh * bytes);
+          for (int h = 0; h < nh; ++h) {
+            uint8_t* sa = a_at(stage, h);
+            const int kc = (kb0 + h) * kTileK;
+            if (up) {  // rows 0-63: gate features m0..m0+63, rows 64-127: the matching up rows
+              tma_load_2d(sa, &tm_w13h, &full[stage], kc, e * 2 * p.I + m0, pol_w);
+              tma_load_2d(sa + kATileBytes / 2, &tm_w13h, &full[stage], kc, e * 2 * p.I + p.I + m0, pol_w);
+            } else {
+              tma_load_2d(sa, &tm_w2, &full[stage], kc, e * p.H + m0, pol_w);
+              tma_load_2d(b_at(stage, h), &tm_act, &full[stage], kc, row0, pol_a);
+            }
           }
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
@@ -181,15 +192,17 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C::kN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb0 = 0; kb0 < kblocks; kb0 += KS) {
           mbar_wait(&full[stage], phase);
           mbar_wait(&bfull[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-          const uint64_t a0 = sdesc_kmajor_sw128(sa);
-          const uint64_t b0 = sdesc_kmajor_sw128(sa + kATileBytes);
+          for (int h = 0; h < min(KS, kblocks - kb0); ++h) {
+            const uint64_t a0 = sdesc_kmajor_sw128(smem_u32(a_at(stage, h)));
+            const uint64_t b0 = sdesc_kmajor_sw128(smem_u32(b_at(stage, h)));
+            const int kb = kb0 + h;
 #pragma unroll
-          for (int k = 0; k < kTileK / 16; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kTileK / 16; ++k) mma_bf16(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+          }
           mma_commit(&empty[stage]);
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
@@ -224,19 +237,23 @@ __global__ void __launch_bounds__(TinyCfg::kThreads, 1)
         }
         const __nv_bfloat16* xs = p.xsrc + j * 8;
         const uint32_t sw = static_cast<uint32_t>((j ^ g) << 4) + static_cast<uint32_t>(g * 128);
-        for (int kb = 0; kb < p.H / kTileK; ++kb) {
+        const int kblocks = p.H / kTileK;
+        for (int kb0 = 0; kb0 < kblocks; kb0 += KS) {
           mbar_wait(&empty[stage], phase ^ 1);
           cp_async_wait_group<S_ - 1>();  // this slot's previous copies (S_ groups ago) landed
-          const uint32_t sb = smem_u32(smem + stage * C::kStageBytes + kATileBytes) + sw;
+          for (int h = 0; h < min(KS, kblocks - kb0); ++h) {
+            const uint32_t sb = smem_u32(b_at(stage, h)) + sw;
 #pragma unroll
-          for (int i = 0; i < RPT; ++i)
-            if (tok[i] >= 0) cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + kb * kTileK, pol_x);
+            for (int i = 0; i < RPT; ++i)
+              if (tok[i] >= 0)
+                cp_async16(sb + i * 8 * 128, xs + static_cast<size_t>(tok[i]) * p.H + (kb0 + h) * kTileK, pol_x);
+          }
           cp_async_arrive_noinc(&bfull[stage]);
           cp_async_commit();
           if (++stage == S_) { stage = 0; phase ^= 1; }
         }
       } else {
-        for (int kb = 0; kb < p.I / kTileK; ++kb) {
+        for (int kb0 = 0; kb0 < p.I / kTileK; kb0 += KS) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive(&bfull[stage]);
           cp_async_commit();
