@@ -11,9 +11,10 @@
 //                   0-63 gate, 64-127 up); the up-lane warps hand their values
 //                   to the gate-lane warps through shared memory for SiLU(g)*u.
 //   DN (e, m0, nt): 128 W2 rows, one tile.
-// Every stage is one 16 KiB weight tile + 16 token rows, so 11 stages keep the
-// same weight bytes in flight per SM as k_experts while twice as many SMs
-// stream. Per output element the K order is unchanged: results are
+// Every stage holds two k-blocks (2 x (16 KiB weight tile + 16 token rows)), 5
+// stages: about the weight bytes in flight per SM of k_experts while twice as
+// many SMs stream, and half the per-stage round trips that pace a decode-size
+// stream (TinyCfg). Per output element the K order is unchanged: results are
 // bit-identical to k_experts on the same token.
 //
 // Warp roles (256 threads): w0 TMA producer + scheduler, w1 MMA issuer, w2 TMEM
