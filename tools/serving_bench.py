@@ -59,15 +59,10 @@ def run_one(stack, name, policy, chunk, target, reqs, focus=None, emit=True, gra
     cfg = ms.types.SchedulerConfig(policy=ms.types.Policy(policy), chunk_size=chunk, group_token_target=target)
     att = None
     if ATTENTION:
-        # pooled KV: slots as long as the longest request, one per request when that fits 48 GB (C3: 33 x
-        # 8208 positions = 27 GB); otherwise as many as fit 64 GB (C5: 19 slots of 33.6 K positions; a
-        # slot is taken when a request is first planned and freed when it finishes, and the modelled B200
-        # run of the same 100-request trace never has more than 8 requests live)
+        # pooled KV: one slot per request, each as long as the longest request, when that fits 48 GB
+        # (C3: 33 x 8208 positions = 27 GB); otherwise per-request caches
         plen = max(r.input_len + r.output_len for r in reqs)
-        per_slot = plen * MODEL.num_layers * 4 * 128 * 2 * 2
-        slots = 0
-        if KV_POOL:
-            slots = len(reqs) if len(reqs) * per_slot <= 48e9 else min(len(reqs), int(64e9 // per_slot))
+        slots = len(reqs) if KV_POOL and len(reqs) * plen * MODEL.num_layers * 4 * 128 * 2 * 2 <= 48e9 else 0
         att = AttentionDense(QWEN3_30B_A3B.hidden, MODEL.num_layers, stack.device, seed=11,
                              pool_slots=slots, pool_len=plen)
     ex = LayeredExecutor(stack, attention=att,
