@@ -43,6 +43,9 @@ UNIT = "us/iter"
 T_DECODE, T_PREFILL = 64, 512
 N_LAYER_SETS = 8
 N_INPUTS = 4
+GRAPHED_E2E_T = 2  # e2e at or below this many tokens: one CUDA graph per call (moe.GraphedHostStep); B200:
+# T=1 / 2 48.4 / 60.5 vs 61.0 / 62.9 us pipelined, but T=4 / 8 / 16 73.5 / 110.2 / 147.0 vs 70.8 / 90.2 / 132.0 —
+# in-graph copies serialise with the layer, where the pipeline overlaps them with neighbouring steps
 
 
 def parse():
@@ -350,9 +353,20 @@ def run_ours(args, rank: int, world: int):
     # ---- end-to-end through the public API with host buffers: every step uploads
     # its input from pinned host memory and downloads its result; the copies of
     # neighbouring steps overlap the layer compute (HostPipeline, two copy streams)
+    # decode sizes (T <= GRAPHED_E2E_T): one CUDA graph per call (GraphedHostStep: H2D, layer, D2H),
+    # since a few KiB of copies cost less than the host side of an event-ordered submit
     y_host = torch.empty((T, s.hidden), dtype=torch.bfloat16, pin_memory=True)
     e2e_layers = layers if world == 1 else None
-    if world == 1:
+    graphed_e2e = world == 1 and T <= GRAPHED_E2E_T
+    if graphed_e2e:
+        from paper_2510_08055_b200.moe import GraphedHostStep
+
+        pipe = GraphedHostStep(dev, T, s.hidden)
+        for i in range(K):  # capture every (layer, input) pair the timed loop uses, outside it
+            pipe.prepare(layers[i % N_LAYER_SETS], xs_host[i % N_INPUTS], y_host)
+        for i in range(3):
+            pipe.submit(layers[i % N_LAYER_SETS], xs_host[i % N_INPUTS], y_host)
+    elif world == 1:
         from paper_2510_08055_b200.moe import HostPipeline
 
         pipe = HostPipeline(dev, T, s.hidden)
@@ -367,7 +381,10 @@ def run_ours(args, rank: int, world: int):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    if e2e_layers is not None:
+    if graphed_e2e:
+        for i in range(K):
+            pipe.submit(layers[i % N_LAYER_SETS], xs_host[i % N_INPUTS], y_host)
+    elif e2e_layers is not None:
         pipe.start(e0)
         for i in range(K):
             pipe.submit(layers[i % N_LAYER_SETS], xs_host[i % N_INPUTS], y_host)
@@ -439,7 +456,9 @@ def run_ours(args, rank: int, world: int):
                          f"({N_LAYER_SETS * s.num_experts * s.bytes_per_expert / 1e9:.1f} GB) rotated per step"},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                 "d2h_bytes_per_step": T * s.hidden * 2,
-                "note": "pipelined: step i's H2D/D2H overlap neighbouring steps' layers (moe.HostPipeline)"
+                "note": ("one CUDA graph per step: H2D of the step's pinned input, the layer, D2H of y "
+                         "(moe.GraphedHostStep), steps back to back" if graphed_e2e else
+                         "pipelined: step i's H2D/D2H overlap neighbouring steps' layers (moe.HostPipeline)")
                         if world == 1 else "one forward_host per step (H2D, EP layer, D2H), back to back"},
         "e2e_latency": {"value": lat_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": T * s.hidden * 2,
                         "d2h_bytes_per_step": T * s.hidden * 2,

@@ -295,6 +295,56 @@ class HostPipeline:
             comp.wait_event(e)
 
 
+class GraphedHostStep:
+    """End-to-end calls from pinned host buffers as ONE CUDA graph per call: the H2D copy of the
+    caller's input, the layer, the D2H copy into the caller's output — for decode-size batches, where
+    the copies are a few KiB and the host cost of an event-ordered submit (HostPipeline: ~25 us of
+    stream / event / ctypes calls) is comparable to the layer itself. A graph is captured on first use
+    per (layer, x_host, y_host) buffer triple and replayed on the current stream afterwards; the
+    captured addresses stay valid while those buffers live and the layer's workspace is not regrown
+    (a call with a larger T than any before it)."""
+
+    def __init__(self, device: torch.device, T: int, H: int):
+        self.device = device
+        self.xd = torch.empty((T, H), dtype=torch.bfloat16, device=device)
+        self.yd = torch.empty((T, H), dtype=torch.bfloat16, device=device)
+        self.pool = torch.cuda.graph_pool_handle()
+        self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+
+    def _body(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        self.xd.copy_(x_host, non_blocking=True)
+        layer.forward(self.xd, out=self.yd)
+        y_host.copy_(self.yd, non_blocking=True)
+
+    def prepare(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        """Capture the graph of this buffer triple now (outside any timed region)."""
+        require(not x_host.is_cuda and not y_host.is_cuda and x_host.is_pinned() and y_host.is_pinned(),
+                "GraphedHostStep expects pinned host tensors")
+        require(tuple(x_host.shape) == tuple(self.xd.shape) and tuple(y_host.shape) == tuple(self.yd.shape),
+                "GraphedHostStep: shape differs from the captured one")
+        key = (id(layer), x_host.data_ptr(), y_host.data_ptr())
+        if key in self.graphs:
+            return
+        cur = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            self._body(layer, x_host, y_host)  # warm-up off the capture: workspace, kernel attributes
+            g.capture_begin(pool=self.pool)
+            self._body(layer, x_host, y_host)
+            g.capture_end()
+        cur.wait_stream(side)
+        self.graphs[key] = g
+
+    def submit(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        g = self.graphs.get((id(layer), x_host.data_ptr(), y_host.data_ptr()))
+        if g is None:
+            self.prepare(layer, x_host, y_host)
+            g = self.graphs[(id(layer), x_host.data_ptr(), y_host.data_ptr())]
+        g.replay()
+
+
 def layer_from_seed(shape: MoEShape, seed: int, device: str = "cuda", tie_break: bool = True) -> GpuMoE:
     """Random-init layer on the dyadic router grid (see synthetic.py)."""
     from .synthetic import expert_weights, router_weight

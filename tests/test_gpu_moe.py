@@ -303,6 +303,28 @@ def test_host_pipeline_matches_device_forward(cuda):
         assert torch.equal(y, ref.cpu())
 
 
+@pytest.mark.parametrize("T", [1, 8])
+def test_graphed_host_step_matches_device_forward(cuda, T):
+    """GraphedHostStep (one CUDA graph per call: H2D, the one-launch decode layer, D2H) returns exactly
+    the device forward's outputs, for two layers, several pinned inputs and repeated replays."""
+    from paper_2510_08055_b200.moe import GraphedHostStep
+
+    s = QWEN3_30B_A3B
+    layers = [make(s, seed, cuda)[3] for seed in (0, 7)]
+    xs = [router_tokens(T, s.hidden, 300 + i).pin_memory() for i in range(3)]
+    ys = [torch.empty((T, s.hidden), dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    step = GraphedHostStep(cuda, T, s.hidden)
+    for rep in range(2):
+        for i, (x, y) in enumerate(zip(xs, ys)):
+            y.zero_()
+            step.submit(layers[(i + rep) % 2], x, y)
+            torch.cuda.synchronize()
+            ref, _ = layers[(i + rep) % 2](x.to(cuda))
+            torch.cuda.synchronize()
+            assert torch.equal(y, ref.cpu()), (rep, i)
+    assert len(step.graphs) == 6
+
+
 @pytest.mark.parametrize("knob", ["LPMOE_FUSED_ROUTE=1", "LPMOE_FUSED_COMBINE=1", "LPMOE_GATHER=1", "LPMOE_GATHER=0",
                                   "LPMOE_PAIR=0", "LPMOE_PAIR_GATHER=1", "LPMOE_TINY=0",
                                   "LPMOE_SCAN_SLOTS=0", "LPMOE_DECODE=0", "LPMOE_DECODE_W2_WARM=0",
