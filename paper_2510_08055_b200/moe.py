@@ -309,7 +309,8 @@ class GraphedHostStep:
         self.xd = torch.empty((T, H), dtype=torch.bfloat16, device=device)
         self.yd = torch.empty((T, H), dtype=torch.bfloat16, device=device)
         self.pool = torch.cuda.graph_pool_handle()
-        self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+        # key -> (graph, layer, x_host, y_host): the references keep every captured address alive
+        self.graphs: dict[tuple, tuple] = {}
 
     def _body(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> None:
         self.xd.copy_(x_host, non_blocking=True)
@@ -335,14 +336,13 @@ class GraphedHostStep:
             self._body(layer, x_host, y_host)
             g.capture_end()
         cur.wait_stream(side)
-        self.graphs[key] = g
+        self.graphs[key] = (g, layer, x_host, y_host)
 
     def submit(self, layer: "GpuMoE", x_host: torch.Tensor, y_host: torch.Tensor) -> None:
-        g = self.graphs.get((id(layer), x_host.data_ptr(), y_host.data_ptr()))
-        if g is None:
+        key = (id(layer), x_host.data_ptr(), y_host.data_ptr())
+        if key not in self.graphs:
             self.prepare(layer, x_host, y_host)
-            g = self.graphs[(id(layer), x_host.data_ptr(), y_host.data_ptr())]
-        g.replay()
+        self.graphs[key][0].replay()
 
 
 def layer_from_seed(shape: MoEShape, seed: int, device: str = "cuda", tie_break: bool = True) -> GpuMoE:
