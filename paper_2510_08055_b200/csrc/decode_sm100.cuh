@@ -521,7 +521,10 @@ __global__ void __launch_bounds__(DecodeCfg::kThreads, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C::kN;
 #ifndef LP_DECODE_MMA_BATCH
-#define LP_DECODE_MMA_BATCH 4  // k-blocks (B200, KS = 1: T=1 / 16 30.3 / 133.7-134.5 vs 30.8-31.1 / 136.6 us with 1)
+// k-blocks waited for together. KS = 1: 4 (T=1 / 16 30.3 / 133.7-134.5 vs 30.8-31.1 / 136.6 us with 1);
+// KS = 2: 2, i.e. one stage (T=1 / 2 / 8 / 16 28.7 / 38.8 / 86.9 / 130.7 vs 29.7 / 39.9 / 87.7 / 132.5 us
+// with 4 and 33.1 / 44.6 / 96.7 / 145.6 with 6; profiles/r02/probe/bench_mma_batch.txt)
+#define LP_DECODE_MMA_BATCH (KS == 1 ? 4 : 2)
 #endif
         constexpr int MB = (LP_DECODE_MMA_BATCH + KS - 1) / KS;  // stages waited for together, then issued back to back
         for (int s0 = 0; s0 < nst; s0 += MB) {
