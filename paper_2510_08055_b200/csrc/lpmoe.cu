@@ -618,9 +618,10 @@ int launch_decode(const void* x, const void* wr, const void* w13, const void* w2
     if ((rc = make_tmap(&tm_w2r[i], w2, static_cast<uint64_t>(E) * H, I, 8u << i))) return rc;
   const int smem = ks == 1 ? lp::DecodeRing<1>::kSmemBytes : lp::DecodeRing<2>::kSmemBytes;
   static const int forced_cs = env_int("LPMOE_DECODE_CS", 0);
-  // B200 (profiles/r02/decode_cs.jsonl): 4-CTA clusters (132 SMs, half the Wr bytes per CTA) win at T <= 3
-  // (T=1 30.6 vs 33.2 us, T=2 41.2 vs 44.5), pairs (148 SMs streaming) from T=4 (58.3 vs 60.1)
-  const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 3 ? 4 : 2);
+  // B200, two-k-block ring (profiles/r02/probe/decode_cs_ks2.txt): 4-CTA clusters (132 SMs, half the Wr
+  // bytes per CTA) win up to T=12 (T=1 28.4 vs 30.8 us, T=4 54.5 vs 57.5, T=8 85.0 vs 86.3, T=12 111.6 vs
+  // 112.4), pairs (148 SMs streaming) at T=16 (130.2 vs 130.9); with the one-k-block ring pairs won from T=4
+  const int cs = forced_cs == 2 || forced_cs == 4 ? forced_cs : (T <= 12 ? 4 : 2);
   auto kern = cs == 4 ? (ks == 1 ? lp::k_decode<4, 1> : lp::k_decode<4, 2>)
                       : (ks == 1 ? lp::k_decode<2, 1> : lp::k_decode<2, 2>);
   if ((rc = set_smem(kern, smem))) return rc;
